@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: bin_by_coordinates -> binned_select_knn forward ->
+backward (BASELINE.json metric: N=1M, d=4, k=40, fwd+bwd; % of HBM roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config north_star|A|B|C|D|E]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N   (N > 1)
+    python bench.py --impl reference     (the reference's own CPU path, rank 0)
+
+Workload (default ``north_star``): one step = one pass of the path over one
+event of 1,000,000 uniform points in [0,1)^4 (the reference's generator,
+seed 3 + rank, cast to float32), k = 40, fixed upstream gradient for the
+backward.  Multi-GPU = event sharding by row splits, one event per GPU (weak
+scaling), no collective in the data path; timings are all-gathered and the
+max over ranks is reported.  Inputs are resident in HBM when the timed region
+starts; L2 is flushed (256 MiB write) before every step.  ``e2e`` repeats the
+measurement with pinned HOST buffers and the host<->device copies inside the
+timed region.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "binned kNN graph-build ms & queries/s, N=1M d=4 k=40, fwd+bwd; % HBM roofline"
+
+# reference candidate counts C_total (the reference algorithm at
+# the reference n_bins), used in the algorithmic byte model.
+C_TOTAL = {"A": 8.6e5, "B": 3.68e9, "north_star": 7.47e8, "C": 1.81e11, "D": 4.51e9,
+           "E": 3.31e8}
+
+
+def algorithmic_bytes(n, d, k, c_total):
+    """B_fwd = 4Nd + 4d*C_total + 8Nk; B_bwd = 8Nk + 8Ndk + 8Nd."""
+    b_fwd = 4 * n * d + 4 * d * c_total + 8 * n * k
+    b_bwd = 8 * n * k + 8 * n * d * k + 8 * n * d
+    return b_fwd, b_bwd
+
+
+def load_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic(config):
+    """dram bytes/launch of the search kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as fh:
+            data = json.load(fh)
+        return data[config]["k_knn_fwd"]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the timed loop runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.FIELDS,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                return
+            self._stop.wait(0.05)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def workload(config, rank, world):
+    from paper_2511_10442_b200.datasets import CONFIGS, generate_dataset
+    n, d, splits, k, dist, seed = CONFIGS[config]
+    if config == "D":
+        # strong scaling: the 64-event batch is sharded by row splits
+        from paper_2511_10442_b200 import sharding
+        coords, off = generate_dataset(n, d, splits, seed, dist)
+        sh = sharding.shard(off, rank, world)
+        n_bins = sharding.global_n_bins(off, k, d)
+        c = coords[sh.vertex_lo:sh.vertex_hi].astype(np.float32)
+        return c, sh.local_offsets, k, n_bins, "strong", \
+            f"D: 64 events x 100k points (events {sh.event_lo}..{sh.event_hi - 1} on rank {rank})"
+    # weak scaling: one event per GPU
+    coords, off = generate_dataset(n, d, splits, seed + rank, dist)
+    from paper_2511_10442_b200.binning import compute_n_bins, default_bin_dims
+    n_bins = compute_n_bins(int(np.diff(off).max()), k, default_bin_dims(d))
+    desc = {"north_star": "north_star: 1 event x 1,000,000 uniform points per GPU, d=4, k=40",
+            "A": "A: 10k points d=3 k=16", "B": "B: 200k clustered points d=4 k=40",
+            "C": "C: 1M points d=10 k=64", "E": "E: 500k points d=4 k=40"}[config]
+    return coords.astype(np.float32), off, k, n_bins, "weak", desc
+
+
+def cpu_reference_sample(coords32, offsets, k, n_bins, sample, seed=0):
+    """The reference's own CPU path (oracle/_ref = its compiled _binned_cy
+    kernels; backward = the oracle's restatement of its numpy knn_backward)
+    timed on a query sample.  Returns (seconds extrapolated to all queries,
+    details dict)."""
+    from oracle import oracle as O  # cpu_baseline leg only
+    ref = O.load_ref_kernels()
+    kind = "reference" if ref is not None else "port"
+    c64 = coords32.astype(np.float64)
+    n, n_c = c64.shape
+    d_bin = min(n_c, 5)
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    if ref is not None:
+        bi, so, bb, mins, widths = ref.build_index(c64, offsets, d_bin, n_bins)
+    else:
+        bi, so, bb, mins, widths = O.build_index(c64, offsets, d_bin, n_bins)
+    t_build = time.perf_counter() - t0
+    rng = np.random.default_rng(seed)
+    rows = rng.choice(n, size=min(sample, n), replace=False)
+    mask = np.zeros(n, np.int8)      # role 0: candidate only
+    mask[rows] = 3                   # sampled rows run their query
+    out_i = np.empty((n, k), np.int32)
+    out_d = np.empty((n, k), np.float64)
+    bc = np.full(d_bin, n_bins, np.int64)
+    t0 = time.perf_counter()
+    if ref is not None:
+        ref.binned_knn(c64, bi, so, bb, bc, widths.min(axis=1).copy(), mask, True, 0.0, False,
+                       False, k, out_i, out_d, threads)
+    else:
+        O.lib().orc_binned_knn_refslot  # noqa: B018
+        oi, od = O.knn_refslot(c64, offsets, k, dir_mask=mask, n_bins=n_bins, threads=threads)
+    t_search = time.perf_counter() - t0
+    up = rng.standard_normal((len(rows), k))
+    t0 = time.perf_counter()
+    O.knn_backward_numpy(c64, out_i[rows], up, rows)
+    t_bwd = time.perf_counter() - t0
+    scale = n / len(rows)
+    total = t_build + (t_search + t_bwd) * scale
+    return total, {"kind": kind, "cores": threads, "t_build_s": t_build,
+                   "t_search_sample_s": t_search, "t_bwd_sample_s": t_bwd,
+                   "sample": (f"{len(rows)} of {n} queries (DirectionMask roles 3/0), search "
+                              f"x{scale:.0f} + full build_index; fwd = reference compiled "
+                              f"_binned_cy on {threads} threads, bwd = numpy knn_backward "
+                              "restatement (1 core)")}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    coords, off, k, n_bins, scaling, desc = workload(args.config, 0, 1)
+    n = coords.shape[0]
+    sample = args.ref_sample
+    for _ in range(max(args.warmup, 0)):
+        cpu_reference_sample(coords, off, k, n_bins, max(sample // 10, 100), seed=1)
+    times = []
+    det = None
+    for s in range(args.steps):
+        tt, det = cpu_reference_sample(coords, off, k, n_bins, sample, seed=100 + s)
+        times.append(tt)
+    t = float(np.mean(times))
+    value = n / t
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": scaling,
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "n_points": n, "k": k, "n_bins": n_bins},
+            "cpu_baseline": {"value": value, "unit": "queries/s", "cores": det["cores"],
+                             "kind": det["kind"], "sample": det["sample"]},
+            "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="north_star", choices=["north_star", "A", "B", "C", "D", "E"])
+    ap.add_argument("--ref-sample", type=int, default=10_000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-flush", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    import paper_2511_10442_b200 as fg
+    from paper_2511_10442_b200 import _lib, ops, sharding
+    _lib.load()
+
+    coords_np, off_np, k, n_bins, scaling, desc = workload(args.config, rank, world)
+    n, d = coords_np.shape
+    d_bin = min(d, 5)
+    rng = np.random.default_rng(1000 + rank)
+    up_np = rng.standard_normal((n, k)).astype(np.float32)
+    coords = torch.from_numpy(coords_np).to(dev)
+    rs = torch.from_numpy(off_np).to(dev)
+    up = torch.from_numpy(up_np).to(dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(c, u):
+        bi, so, bb, mins, widths, sc = ops.bin_by_coordinates(c, rs, d_bin, n_bins)
+        ev_knn = torch.cuda.Event(enable_timing=True)
+        ev_knn.record(stream)
+        idx, d2 = ops.binned_select_knn(c, rs, bi, so, bb, mins, widths, sc, k, d_bin, n_bins,
+                                        None, None, False, False)
+        ev_bwd = torch.cuda.Event(enable_timing=True)
+        ev_bwd.record(stream)
+        g = ops.binned_select_knn_grad(u, idx, c)
+        return idx, d2, g, ev_knn, ev_bwd
+
+    for _ in range(max(args.warmup, 3) if args.warmup > 0 else 0):
+        step(coords, up)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    sampler = ClockSampler(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[0])
+                           if os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")[0].isdigit()
+                           else local)
+    launches0 = _lib.launch_count()
+    t_step = t_bin = t_knn = t_bwd = 0.0
+    with sampler:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        for _ in range(args.steps):
+            if not args.no_flush:
+                flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e3 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            idx, d2, g, e1, e2 = step(coords, up)
+            e3.record(stream)
+            e3.synchronize()
+            t_step += e0.elapsed_time(e3)
+            t_bin += e0.elapsed_time(e1)
+            t_knn += e1.elapsed_time(e2)
+            t_bwd += e2.elapsed_time(e3)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    launches = _lib.launch_count() - launches0
+    clocks = sampler.summary()
+
+    # e2e through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        h_coords = torch.from_numpy(coords_np).pin_memory()
+        h_up = torch.from_numpy(up_np).pin_memory()
+        h_idx = torch.empty((n, k), dtype=torch.int32).pin_memory()
+        h_d2 = torch.empty((n, k), dtype=torch.float32).pin_memory()
+        h_g = torch.empty((n, d), dtype=torch.float32).pin_memory()
+        t_e2e = 0.0
+        e2e_steps = max(1, min(args.steps, 10))
+        for it in range(e2e_steps + 1):
+            if not args.no_flush:
+                flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            c = h_coords.to(dev, non_blocking=True)
+            u = h_up.to(dev, non_blocking=True)
+            idx, d2, g, _, _ = step(c, u)
+            h_idx.copy_(idx, non_blocking=True)
+            h_d2.copy_(d2, non_blocking=True)
+            h_g.copy_(g, non_blocking=True)
+            e1.record(stream)
+            e1.synchronize()
+            if it > 0:  # first iteration warms the pinned paths
+                t_e2e += e0.elapsed_time(e1)
+        e2e_ms = t_e2e / e2e_steps
+        h2d = h_coords.numel() * 4 + h_up.numel() * 4
+        d2h = h_idx.numel() * 4 + h_d2.numel() * 4 + h_g.numel() * 4
+        e2e = [e2e_ms, h2d, d2h]
+
+    per_rank = [t_step / args.steps, t_bin / args.steps, t_knn / args.steps, t_bwd / args.steps,
+                n, e2e[0] if e2e else 0.0]
+    allr = sharding.gather_floats(per_rank)
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
+    ms = float(allr[:, 0].max())
+    total_q = float(allr[:, 4].sum())
+    value = total_q / (ms * 1e-3)
+    peak, peak_src = load_peak()
+    c_total = C_TOTAL[args.config]
+    if args.config == "D":
+        c_total = C_TOTAL["D"] * (n / 6_400_000)
+    b_fwd, b_bwd = algorithmic_bytes(n, d, k, c_total)
+    t_knn_ms = float(allr[0, 2])
+    achieved = b_fwd / (t_knn_ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (reference generate_dataset, seed per rank, cast to float32)",
+        "config": {"workload": desc, "n_points_per_gpu": n, "d": d, "k": k, "n_bins": n_bins,
+                   "d_bin": d_bin, "events": world if scaling == "weak" else 64,
+                   "l2": "no flush" if args.no_flush else "flushed (256 MiB write) before every step",
+                   "precision": "fp32 distance filter, float64 exact epilogue / gradient sums"},
+        "breakdown_ms": {"bin_by_coordinates": float(allr[0, 1]), "knn_fwd": t_knn_ms,
+                         "knn_bwd": float(allr[0, 3])},
+        "roofline": {"bound": "hbm", "kernel": "k_knn_fwd", "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": load_traffic(args.config),
+                     "peak_source": peak_src,
+                     "bytes_model": "SURVEY 8(d) B_fwd = 4Nd + 4d*C_total + 8Nk "
+                                    f"(C_total={c_total:.3g}) per launch",
+                     "step_frac": (b_fwd + b_bwd) / (ms * 1e-3) / 1e9 / peak},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+    }
+    if e2e:
+        e2e_ms = float(allr[:, 5].max())
+        line["e2e"] = {"value": total_q / (e2e_ms * 1e-3), "unit": "queries/s",
+                       "h2d_bytes_per_step": int(e2e[1]), "d2h_bytes_per_step": int(e2e[2]),
+                       "ms_per_step": e2e_ms}
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            tt, det = cpu_reference_sample(coords_np, off_np, k, n_bins, args.ref_sample)
+            line["cpu_baseline"] = {"value": n / tt, "unit": "queries/s", "cores": det["cores"],
+                                    "kind": det["kind"], "sample": det["sample"]}
+        except Exception as exc:  # the baseline must not kill the GPU number
+            line["cpu_baseline"] = {"value": None, "unit": "queries/s", "cores": os.cpu_count(),
+                                    "kind": "unavailable", "sample": repr(exc)}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

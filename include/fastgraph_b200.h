@@ -1,0 +1,156 @@
+/*
+ * fastgraph_b200.h -- C ABI of the B200-native bin-partitioned exact kNN.
+ *
+ * The drop-in boundary.  Every entry point takes plain device pointers and
+ * sizes, enqueues its kernels on the given CUDA stream (`stream` is a
+ * cudaStream_t / CUstream passed as void*; NULL = legacy default stream),
+ * never synchronises the host and never allocates: outputs and scratch are
+ * caller-owned (the Python layer uses torch's caching allocator).  Every
+ * function returns 0 on success, a negative FG_ERR_* for a bad argument
+ * (checked before any launch, nothing enqueued), or a positive cudaError_t
+ * from the launch.  fg_error_string() describes a code.
+ *
+ * Each entry point names the reference interface it replaces; paths are
+ * relative to /root/reference/pkg/src/gridknn ("pyx" = _kernels/_binned_cy.pyx).
+ * The reference's backend protocol (pyx NAME/build_index/ring_cells/
+ * binned_knn/brute_knn, selected by _kernels/__init__.py:23-38) is host numpy;
+ * paper_2511_10442_b200/backend.py adapts it onto this ABI, and
+ * paper_2511_10442_b200/ops.py registers the torch ops (fastgraph::*) on it.
+ *
+ * Conventions
+ *  - coordinates are float32, row-major (n, n_coords), 1 <= n_coords <= 16;
+ *  - row_splits are int64 offsets (n_splits + 1), starting at 0, non-decreasing,
+ *    ending at n (G/core.py:49-98); empty splits are legal;
+ *  - neighbour indices are int32 original vertex ids, n < 2^31 (G/knn.py:51);
+ *  - distances are squared Euclidean over ALL n_coords dims (pyx:32-48).
+ *  - parity contract: rows are sorted by (float64 d2 computed exactly as the
+ *    reference does, original index) -- lower index wins ties; slot 0 is the
+ *    vertex itself with d2 0; unfilled slots are (-1, 0).
+ */
+#ifndef FASTGRAPH_B200_H
+#define FASTGRAPH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FG_ABI_VERSION 1
+
+enum fg_status {
+    FG_OK = 0,
+    FG_ERR_BAD_K = -1,          /* k < 1 or too large (G/knn.py:48-50 BadKError)       */
+    FG_ERR_BAD_SHAPE = -2,      /* bad sizes / dims (G/errors.py BadShapeError)         */
+    FG_ERR_TOO_FEW_DIMS = -3,   /* d_bin outside [1,5] or > n_coords (TooFewDimsError) */
+    FG_ERR_WORKSPACE = -4,      /* workspace smaller than fg_*_workspace_size()         */
+    FG_ERR_NULL = -5,           /* required pointer is NULL                             */
+    FG_ERR_TOO_MANY_DIMS = -6,  /* n_coords > 16                                        */
+    FG_ERR_BAD_RADIUS = -7      /* max_radius2 < 0 (G/knn.py:57-58 BadKError)          */
+};
+
+/* Option bits for fg_knn_fwd (mirror KnnOptions, G/knn.py:34-45, and the
+ * exhaustive_rings flag of binned_select_knn, G/knn.py:82-84). */
+#define FG_KNN_USE_DIRECTION 0x1 /* dir_mask is read: roles 0/2 skip the query, 1/2 hide the
+                                    candidate (pyx:210-211, 265-266; G/core.py:181-184)      */
+#define FG_KNN_USE_MAX_R2 0x2    /* drop candidates with d2 > max_radius2 (boundary kept)  */
+#define FG_KNN_EXHAUSTIVE 0x4    /* no early stop and no pruning (diagnostic, same result) */
+#define FG_KNN_D2_F64 0x8        /* out_d2 is double (bit-exact reference float64 d2);
+                                    otherwise float (= float32 of the reference d2)         */
+
+/* Reducer codes for the GravNet aggregation (G/gravnet.py:26, order = blocks). */
+#define FG_REDUCE_MEAN 0
+#define FG_REDUCE_MAX 1
+
+/* ---------------------------------------------------------------- binning */
+
+/* Scratch bytes needed by fg_bin_by_coordinates for these sizes. */
+int fg_bin_workspace_size(int64_t n, int32_t n_splits, int32_t d_bin, int32_t n_bins,
+                          size_t *bytes);
+
+/* bin_by_coordinates.  Replaces build_bin_index -> kb.build_index
+ * (G/binning.py:136-170 -> pyx:66-139) and yields bit-identical arrays:
+ *   bin_idx[n]        int64  global cell s*n_bins^d_bin + row-major flat cell
+ *   sort_order[n]     int32  vertices cell by cell, ascending id within a cell
+ *                            (the reference's stable counting sort)
+ *   bin_bounds[S*n_bins^d_bin + 1] int32  sort_order range of every cell
+ *   dim_mins[S*d_bin], widths[S*d_bin] float64 (empty split: 0 / 1.0)
+ * plus the B200 layout the search reads:
+ *   sorted_coords[n * coord_stride] float32, coords gathered in sort_order,
+ *   zero padded to coord_stride = 4*ceil(n_coords/4) (16-byte vectors).
+ * n_bins is the caller's (host) choice; the reference rule lives in the host
+ * layer (G/binning.py:40-62,159-162). */
+int fg_bin_by_coordinates(const float *coords, int64_t n, int32_t n_coords,
+                          const int64_t *row_splits, int32_t n_splits, int32_t d_bin,
+                          int32_t n_bins, int64_t *bin_idx, int32_t *sort_order,
+                          int32_t *bin_bounds, double *dim_mins, double *widths,
+                          float *sorted_coords, void *workspace, size_t workspace_bytes,
+                          void *stream);
+
+/* index_replacer: io[i] = lut[io[i]] for io[i] >= 0, negatives kept.  The
+ * reference does this implicitly (u = sort_order[p], pyx:262); fg_knn_fwd
+ * already emits original ids, this is the standalone op. */
+int fg_index_replacer(int32_t *io, int64_t n, const int32_t *lut, int64_t lut_n, void *stream);
+
+/* ---------------------------------------------------------------- search */
+
+/* binned_select_knn forward.  Replaces binned_select_knn -> kb.binned_knn
+ * (G/knn.py:82-115 -> pyx:303-329, _search_one pyx:188-300).  Reads the
+ * arrays of fg_bin_by_coordinates; writes out_idx[n*k] (int32) and
+ * out_d2[n*k] (float or double, FG_KNN_D2_F64) at the ORIGINAL row of each
+ * vertex.  dir_mask (int8, original order) is read only with
+ * FG_KNN_USE_DIRECTION.  k counts the vertex itself (1 <= k <= 960). */
+int fg_knn_fwd(const float *sorted_coords, const int32_t *sort_order, const int64_t *bin_idx,
+               const int32_t *bin_bounds, const int64_t *row_splits, const double *dim_mins,
+               const double *widths, int64_t n, int32_t n_coords, int32_t n_splits,
+               int32_t d_bin, int32_t n_bins, int32_t k, const int8_t *dir_mask,
+               double max_radius2, uint32_t flags, int32_t *out_idx, void *out_d2,
+               void *stream);
+
+/* ---------------------------------------------------------------- backward */
+
+int fg_knn_bwd_workspace_size(int64_t n, int32_t n_coords, size_t *bytes);
+
+/* binned_select_knn backward.  Replaces knn_backward (G/knn.py:135-168):
+ * for every valid non-self slot (v,s) -> u with upstream g = grad_d2[v,s],
+ * grad[v] += 2g(x_v - x_u) and grad[u] -= 2g(x_v - x_u).  Terms are formed
+ * exactly in float64 and accumulated in float64; grad_coords is float32
+ * (or double with grad_is_f64). */
+int fg_knn_bwd(const float *coords, int64_t n, int32_t n_coords, const int32_t *idx, int32_t k,
+               const float *grad_d2, void *grad_coords, int32_t grad_is_f64, void *workspace,
+               size_t workspace_bytes, void *stream);
+
+/* ---------------------------------------------------------------- GravNet */
+
+/* gravnet_aggregate.  Replaces G/gravnet.py:64-97: per vertex, weights
+ * w = exp(-scale*d2) over valid slots (idx >= 0, slot 0 only with
+ * include_self), reducers applied in order (FG_REDUCE_*), one F-wide block
+ * each: out[n, F*n_reducers] float32.  Arithmetic in float64. */
+int fg_gravnet_fwd(const float *feats, int64_t n, int32_t n_feats, const int32_t *idx,
+                   const float *d2, int32_t k, double weight_scale, const int32_t *reducers,
+                   int32_t n_reducers, int32_t include_self, float *out, void *stream);
+
+int fg_gravnet_bwd_workspace_size(int64_t n, int32_t n_feats, size_t *bytes);
+
+/* gravnet_aggregate_backward.  Replaces G/gravnet.py:100-150 ->
+ * (grad_feats[n,F] float32, grad_d2[n,k] float32); max blocks route to the
+ * lowest arg-max slot. */
+int fg_gravnet_bwd(const float *feats, int64_t n, int32_t n_feats, const int32_t *idx,
+                   const float *d2, int32_t k, double weight_scale, const int32_t *reducers,
+                   int32_t n_reducers, int32_t include_self, const float *upstream,
+                   float *grad_feats, float *grad_d2, void *workspace, size_t workspace_bytes,
+                   void *stream);
+
+/* ---------------------------------------------------------------- misc */
+
+const char *fg_error_string(int code);
+int fg_abi_version(void);
+/* Kernels this library has launched since load (evidence for bench.py). */
+uint64_t fg_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FASTGRAPH_B200_H */

@@ -1,0 +1,585 @@
+// fg_bin.cu -- bin_by_coordinates for sm_100a (replaces pyx:66-139).
+//
+// K1 k_bbox          per-split min/max over the first d_bin dims: block
+//                    reduction per (block chunk, split segment), one ordered-
+//                    uint atomicMin/Max per block and dim.
+// K1b k_bbox_final   dim_mins / widths exactly as pyx:114-118 (float64).
+// K2 k_assign        cell = floor((x - min) / w) in float64, clamped, row-major
+//                    flat, global id; warp-aggregated (match_any) histogram.
+// K3 k_scan          single-pass decoupled-look-back exclusive scan of the
+//                    histogram -> bin_bounds (+ a cursor copy).  CUB-free.
+// K4 k_scatter       atomic-cursor scatter into sort_order (warp-aggregated,
+//                    warp-local order kept), then the stable fix-up that makes
+//                    sort_order identical to the reference's stable counting
+//                    sort: each cell segment is re-sorted by vertex id --
+//                    k_fix_small (thread per cell, <= 32), k_fix_medium (CTA
+//                    bitonic in smem, <= 4096) and k_fix_big (CTA in-order
+//                    compaction over the split) -- and every segment's
+//                    coordinates are gathered into sorted_coords with 16-byte
+//                    stores (float4 rows padded to 4*ceil(n_c/4)).
+#include "fg_common.cuh"
+
+namespace fg {
+
+std::atomic<uint64_t> g_launches{0};
+
+namespace binning {
+
+constexpr int kMaxBinDims = 5;
+constexpr int kSmallCell = 32;
+constexpr int kMediumCell = 4096;
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+struct BinWs {
+    unsigned* bbox;          // n_splits * d_bin * 2 (ordered min, ordered max)
+    int32_t* cursor;         // n_cells (histogram, then scatter cursor)
+    unsigned long long* st;  // scan tile status words
+    unsigned* counters;      // [0] scan tile ticket, [1] medium count, [2] big count
+    int32_t* medium;         // medium cell list
+    int32_t* big;            // big cell list
+    int64_t n_tiles;
+    int64_t list_cap;
+};
+
+size_t carve(BinWs* w, void* base, int64_t n, int32_t n_splits, int32_t d_bin, int64_t n_cells) {
+    size_t off = 0;
+    char* b = (char*)base;
+    auto take = [&](size_t bytes) {
+        off = align_up(off, 256);
+        char* p = b ? b + off : nullptr;
+        off += bytes;
+        return p;
+    };
+    w->n_tiles = ceil_div(n_cells, kScanTile);
+    w->list_cap = n / (kSmallCell + 1) + 1;
+    w->bbox = (unsigned*)take(sizeof(unsigned) * (size_t)n_splits * d_bin * 2);
+    w->cursor = (int32_t*)take(sizeof(int32_t) * (size_t)n_cells);
+    w->st = (unsigned long long*)take(sizeof(unsigned long long) * (size_t)w->n_tiles);
+    w->counters = (unsigned*)take(sizeof(unsigned) * 4);
+    w->medium = (int32_t*)take(sizeof(int32_t) * (size_t)w->list_cap);
+    w->big = (int32_t*)take(sizeof(int32_t) * (size_t)w->list_cap);
+    return align_up(off, 256);
+}
+
+// ---------------------------------------------------------------- K1
+__global__ void k_bbox_init(unsigned* bbox, int64_t m) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x)
+        bbox[i] = (i & 1) ? 0u : 0xffffffffu;  // even = min slot, odd = max slot
+}
+
+template <int DB>
+__global__ void __launch_bounds__(256) k_bbox(const float* __restrict__ coords, int64_t n, int n_c,
+                                              const int64_t* __restrict__ rs, int n_splits,
+                                              int64_t chunk, unsigned* __restrict__ bbox) {
+    __shared__ float s_mn[8][DB], s_mx[8][DB];
+    int64_t lo = blockIdx.x * chunk;
+    const int64_t hi = min(n, lo + chunk);
+    if (lo >= hi) return;
+    int s = split_of(rs, n_splits, lo);
+    while (lo < hi) {
+        const int64_t seg_end = min(hi, rs[s + 1]);
+        if (seg_end <= lo) {  // empty split
+            ++s;
+            continue;
+        }
+        float mn[DB], mx[DB];
+#pragma unroll
+        for (int d = 0; d < DB; ++d) {
+            mn[d] = __int_as_float(0x7f800000);   // +inf
+            mx[d] = -__int_as_float(0x7f800000);  // -inf
+        }
+        for (int64_t v = lo + threadIdx.x; v < seg_end; v += blockDim.x) {
+#pragma unroll
+            for (int d = 0; d < DB; ++d) {
+                const float x = coords[v * n_c + d];
+                mn[d] = fminf(mn[d], x);
+                mx[d] = fmaxf(mx[d], x);
+            }
+        }
+#pragma unroll
+        for (int d = 0; d < DB; ++d) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                mn[d] = fminf(mn[d], __shfl_xor_sync(FG_FULL_MASK, mn[d], o));
+                mx[d] = fmaxf(mx[d], __shfl_xor_sync(FG_FULL_MASK, mx[d], o));
+            }
+        }
+        const int w = threadIdx.x >> 5;
+        if (lane_id() == 0) {
+#pragma unroll
+            for (int d = 0; d < DB; ++d) {
+                s_mn[w][d] = mn[d];
+                s_mx[w][d] = mx[d];
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x < DB) {
+            const int d = threadIdx.x;
+            float a = s_mn[0][d], b = s_mx[0][d];
+            for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
+                a = fminf(a, s_mn[i][d]);
+                b = fmaxf(b, s_mx[i][d]);
+            }
+            atomicMin(&bbox[((int64_t)s * DB + d) * 2 + 0], float_to_ordered(a));
+            atomicMax(&bbox[((int64_t)s * DB + d) * 2 + 1], float_to_ordered(b));
+        }
+        __syncthreads();
+        lo = seg_end;
+        ++s;
+    }
+}
+
+// pyx:99-118: empty split keeps min 0 / width 1; width = ext / n_bins or 1.0.
+__global__ void k_bbox_final(const unsigned* __restrict__ bbox, const int64_t* __restrict__ rs,
+                             int n_splits, int d_bin, int n_bins, double* __restrict__ mins,
+                             double* __restrict__ widths) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= (int64_t)n_splits * d_bin) return;
+    const int64_t s = i / d_bin;
+    if (rs[s + 1] <= rs[s]) {
+        mins[i] = 0.0;
+        widths[i] = 1.0;
+        return;
+    }
+    const double mn = (double)ordered_to_float(bbox[i * 2 + 0]);
+    const double mx = (double)ordered_to_float(bbox[i * 2 + 1]);
+    const double ext = __dsub_rn(mx, mn);
+    mins[i] = mn;
+    widths[i] = ext > 0.0 ? __ddiv_rn(ext, (double)n_bins) : 1.0;
+}
+
+// ---------------------------------------------------------------- K2
+template <int DB>
+__global__ void __launch_bounds__(256) k_assign(const float* __restrict__ coords, int64_t n, int n_c,
+                                                const int64_t* __restrict__ rs, int n_splits,
+                                                int n_bins, int64_t total,
+                                                const double* __restrict__ mins,
+                                                const double* __restrict__ widths,
+                                                int64_t* __restrict__ bin_idx,
+                                                int32_t* __restrict__ hist) {
+    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool live = v < n;
+    unsigned long long g = ~0ull;
+    if (live) {
+        const int s = split_of(rs, n_splits, v);
+        int64_t flat = 0;
+#pragma unroll
+        for (int d = 0; d < DB; ++d) {
+            const double x = (double)coords[v * n_c + d];
+            const double q = __ddiv_rn(__dsub_rn(x, mins[(int64_t)s * DB + d]),
+                                       widths[(int64_t)s * DB + d]);
+            int64_t c = (int64_t)floor(q);
+            c = c < 0 ? 0 : (c >= n_bins ? n_bins - 1 : c);
+            flat = flat * n_bins + c;
+        }
+        g = (unsigned long long)((int64_t)s * total + flat);
+        bin_idx[v] = (int64_t)g;
+    }
+    // warp-aggregated histogram: one atomic per distinct cell in the warp
+    const unsigned peers = __match_any_sync(FG_FULL_MASK, g);
+    if (live && (__ffs(peers) - 1) == lane_id()) atomicAdd(&hist[g], __popc(peers));
+}
+
+// ---------------------------------------------------------------- K3
+// Exclusive scan of hist[0..m) into out[0..m] (out[m] = grand total) and a
+// copy into cursor[0..m). Status word: bits 62-63 flag (0 invalid, 1 tile
+// aggregate, 2 inclusive prefix), low 32 bits the value.
+__global__ void __launch_bounds__(kScanThreads) k_scan(const int32_t* __restrict__ hist, int64_t m,
+                                                       int32_t* __restrict__ out,
+                                                       int32_t* __restrict__ cursor,
+                                                       unsigned long long* __restrict__ status,
+                                                       unsigned* __restrict__ ticket) {
+    __shared__ int32_t s_items[kScanTile];
+    __shared__ int32_t s_warp[kScanThreads / 32];
+    __shared__ int32_t s_prefix;
+    __shared__ unsigned s_tile;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int64_t base = tile * kScanTile;
+    for (int i = threadIdx.x; i < kScanTile; i += kScanThreads) {
+        const int64_t g = base + i;
+        s_items[i] = g < m ? hist[g] : 0;
+    }
+    __syncthreads();
+    int32_t local[kScanItems];
+    int32_t run = 0;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        local[j] = run;  // exclusive within the thread
+        run += s_items[threadIdx.x * kScanItems + j];
+    }
+    const int lane = lane_id(), w = threadIdx.x >> 5;
+    const int32_t incl = warp_inclusive_scan(run);
+    if (lane == 31) s_warp[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        int32_t x = lane < kScanThreads / 32 ? s_warp[lane] : 0;
+        x = warp_inclusive_scan(x);
+        if (lane < kScanThreads / 32) s_warp[lane] = x;
+    }
+    __syncthreads();
+    const int32_t thread_excl = (incl - run) + (w > 0 ? s_warp[w - 1] : 0);
+    const int32_t tile_total = s_warp[kScanThreads / 32 - 1];
+    // decoupled look-back (warp 0)
+    if (w == 0) {
+        int32_t prefix = 0;
+        if (tile == 0) {
+            if (lane == 0) {
+                __threadfence();
+                atomicExch(&status[0], (2ull << 62) | (unsigned)tile_total);
+            }
+        } else {
+            if (lane == 0) {
+                __threadfence();
+                atomicExch(&status[tile], (1ull << 62) | (unsigned)tile_total);
+            }
+            int64_t end = tile - 1;  // closest predecessor examined by lane 0
+            while (true) {
+                const int64_t idx = end - lane;
+                unsigned long long word = 2ull << 62;  // before tile 0: prefix 0
+                if (idx >= 0) {
+                    do {
+                        word = *((volatile unsigned long long*)&status[idx]);
+                    } while ((word >> 62) == 0);
+                }
+                const unsigned flag = (unsigned)(word >> 62);
+                const int32_t val = idx >= 0 ? (int32_t)(word & 0xffffffffu) : 0;
+                const unsigned pmask = __ballot_sync(FG_FULL_MASK, flag == 2);
+                if (pmask) {
+                    const int first = __ffs(pmask) - 1;
+                    int32_t x = lane <= first ? val : 0;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FG_FULL_MASK, x, o);
+                    prefix += x;
+                    break;
+                }
+                int32_t x = val;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FG_FULL_MASK, x, o);
+                prefix += x;
+                end -= 32;
+            }
+            if (lane == 0) {
+                __threadfence();
+                atomicExch(&status[tile], (2ull << 62) | (unsigned)(prefix + tile_total));
+            }
+        }
+        if (lane == 0) s_prefix = prefix;
+    }
+    __syncthreads();
+    const int32_t pre = s_prefix + thread_excl;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) s_items[threadIdx.x * kScanItems + j] = pre + local[j];
+    __syncthreads();
+    for (int i = threadIdx.x; i < kScanTile; i += kScanThreads) {
+        const int64_t g = base + i;
+        if (g < m) {
+            out[g] = s_items[i];
+            cursor[g] = s_items[i];
+        }
+    }
+    if (base + kScanTile >= m && threadIdx.x == 0) out[m] = s_prefix + tile_total;
+}
+
+// ---------------------------------------------------------------- K4
+__global__ void __launch_bounds__(256) k_scatter(const int64_t* __restrict__ bin_idx, int64_t n,
+                                                 int32_t* __restrict__ cursor,
+                                                 int32_t* __restrict__ sort_order) {
+    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool live = v < n;
+    const unsigned long long g = live ? (unsigned long long)bin_idx[v] : ~0ull;
+    const unsigned peers = __match_any_sync(FG_FULL_MASK, g);
+    const int leader = __ffs(peers) - 1;
+    int32_t base = 0;
+    if (live && leader == lane_id()) base = atomicAdd(&cursor[g], __popc(peers));
+    base = __shfl_sync(FG_FULL_MASK, base, leader);
+    if (live) sort_order[base + __popc(peers & lanemask_lt())] = (int32_t)v;
+}
+
+template <int NV>
+__device__ __forceinline__ void gather_row(const float* __restrict__ coords, int n_c, int32_t v,
+                                           float4* __restrict__ dst) {
+    const float* src = coords + (int64_t)v * n_c;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        float t[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) t[e] = (4 * j + e < n_c) ? src[4 * j + e] : 0.0f;
+        dst[j] = make_float4(t[0], t[1], t[2], t[3]);
+    }
+}
+
+// Thread per cell: sort segments of <= 32 ids (insertion sort), gather coords;
+// longer segments are queued for the CTA-level fix-ups.
+template <int NV>
+__global__ void __launch_bounds__(256) k_fix_small(const int32_t* __restrict__ bounds, int64_t n_cells,
+                                                   int32_t* __restrict__ sort_order,
+                                                   const float* __restrict__ coords, int n_c,
+                                                   float4* __restrict__ sorted,
+                                                   unsigned* __restrict__ counters,
+                                                   int32_t* __restrict__ medium,
+                                                   int32_t* __restrict__ big) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= n_cells) return;
+    const int32_t lo = bounds[c], hi = bounds[c + 1];
+    const int len = hi - lo;
+    if (len == 0) return;
+    if (len > kSmallCell) {
+        if (len > kMediumCell)
+            big[atomicAdd(&counters[2], 1u)] = (int32_t)c;
+        else
+            medium[atomicAdd(&counters[1], 1u)] = (int32_t)c;
+        return;
+    }
+    int32_t ids[kSmallCell];
+    for (int i = 0; i < len; ++i) {
+        int32_t x = sort_order[lo + i];
+        int j = i;
+        while (j > 0 && ids[j - 1] > x) {
+            ids[j] = ids[j - 1];
+            --j;
+        }
+        ids[j] = x;
+    }
+    for (int i = 0; i < len; ++i) {
+        sort_order[lo + i] = ids[i];
+        gather_row<NV>(coords, n_c, ids[i], sorted + (int64_t)(lo + i) * NV);
+    }
+}
+
+template <int NV>
+__global__ void __launch_bounds__(1024) k_fix_medium(const int32_t* __restrict__ bounds,
+                                                     int32_t* __restrict__ sort_order,
+                                                     const float* __restrict__ coords, int n_c,
+                                                     float4* __restrict__ sorted,
+                                                     const unsigned* __restrict__ counters,
+                                                     const int32_t* __restrict__ medium) {
+    __shared__ int32_t s[kMediumCell];
+    const unsigned count = counters[1];
+    for (unsigned it = blockIdx.x; it < count; it += gridDim.x) {
+        const int32_t c = medium[it];
+        const int32_t lo = bounds[c], len = bounds[c + 1] - lo;
+        int p2 = 64;
+        while (p2 < len) p2 <<= 1;
+        for (int i = threadIdx.x; i < p2; i += blockDim.x)
+            s[i] = i < len ? sort_order[lo + i] : 0x7fffffff;
+        __syncthreads();
+        for (int size = 2; size <= p2; size <<= 1)
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                for (int i = threadIdx.x; i < p2 / 2; i += blockDim.x) {
+                    const int a = 2 * stride * (i / stride) + (i % stride), b = a + stride;
+                    const bool up = (a & size) == 0;
+                    const int32_t x = s[a], y = s[b];
+                    if ((x > y) == up) {
+                        s[a] = y;
+                        s[b] = x;
+                    }
+                }
+                __syncthreads();
+            }
+        for (int i = threadIdx.x; i < len; i += blockDim.x) {
+            sort_order[lo + i] = s[i];
+            gather_row<NV>(coords, n_c, s[i], sorted + (int64_t)(lo + i) * NV);
+        }
+        __syncthreads();
+    }
+}
+
+// Huge cells: the members of cell c in ascending id order are exactly the
+// vertices v of its split with bin_idx[v] == c, so one CTA compacts the
+// split range in order (block-wide exclusive scan per chunk).
+template <int NV>
+__global__ void __launch_bounds__(1024) k_fix_big(const int32_t* __restrict__ bounds,
+                                                  const int64_t* __restrict__ bin_idx,
+                                                  const int64_t* __restrict__ rs, int64_t total,
+                                                  int32_t* __restrict__ sort_order,
+                                                  const float* __restrict__ coords, int n_c,
+                                                  float4* __restrict__ sorted,
+                                                  const unsigned* __restrict__ counters,
+                                                  const int32_t* __restrict__ big) {
+    __shared__ int32_t s_warp[32];
+    __shared__ int32_t s_run;
+    const unsigned count = counters[2];
+    for (unsigned it = blockIdx.x; it < count; it += gridDim.x) {
+        const int32_t c = big[it];
+        const int64_t s = c / total;
+        const int32_t lo = bounds[c];
+        const int64_t v0 = rs[s], v1 = rs[s + 1];
+        if (threadIdx.x == 0) s_run = 0;
+        __syncthreads();
+        for (int64_t b = v0; b < v1; b += blockDim.x) {
+            const int64_t v = b + threadIdx.x;
+            const int flag = (v < v1 && bin_idx[v] == c) ? 1 : 0;
+            const int w = threadIdx.x >> 5, lane = lane_id();
+            const int incl = warp_inclusive_scan(flag);
+            if (lane == 31) s_warp[w] = incl;
+            __syncthreads();
+            if (w == 0) {
+                int x = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0;
+                x = warp_inclusive_scan(x);
+                s_warp[lane] = x;
+            }
+            __syncthreads();
+            const int excl = incl - flag + (w > 0 ? s_warp[w - 1] : 0);
+            const int run = s_run;
+            if (flag) sort_order[lo + run + excl] = (int32_t)v;
+            __syncthreads();
+            if (threadIdx.x == 0) s_run = run + s_warp[(blockDim.x >> 5) - 1];
+            __syncthreads();
+        }
+        const int32_t len = bounds[c + 1] - lo;
+        for (int i = threadIdx.x; i < len; i += blockDim.x)
+            gather_row<NV>(coords, n_c, sort_order[lo + i], sorted + (int64_t)(lo + i) * NV);
+        __syncthreads();
+    }
+}
+
+template <int NV>
+int launch_fixups(const int32_t* bounds, int64_t n_cells, int32_t* sort_order, const int64_t* bin_idx,
+                  const int64_t* rs, int64_t total, const float* coords, int n_c, float* sorted,
+                  const BinWs& w, cudaStream_t st) {
+    float4* s4 = reinterpret_cast<float4*>(sorted);
+    if (n_cells > 0) {
+        k_fix_small<NV><<<(unsigned)ceil_div(n_cells, 256), 256, 0, st>>>(
+            bounds, n_cells, sort_order, coords, n_c, s4, w.counters, w.medium, w.big);
+        FG_TRY(launched(st));
+    }
+    k_fix_medium<NV><<<296, 1024, 0, st>>>(bounds, sort_order, coords, n_c, s4, w.counters,
+                                           w.medium);
+    FG_TRY(launched(st));
+    k_fix_big<NV><<<148, 1024, 0, st>>>(bounds, bin_idx, rs, total, sort_order, coords, n_c, s4,
+                                        w.counters, w.big);
+    return launched(st);
+}
+
+template <int DB>
+int launch_bin_core(const float* coords, int64_t n, int n_c, const int64_t* rs, int n_splits,
+                    int n_bins, int64_t total, double* mins, double* widths, int64_t* bin_idx,
+                    const BinWs& w, cudaStream_t st) {
+    const int64_t m = (int64_t)n_splits * DB * 2;
+    k_bbox_init<<<(unsigned)ceil_div(m, 256), 256, 0, st>>>(w.bbox, m);
+    FG_TRY(launched(st));
+    if (n > 0) {
+        const int64_t chunk = 8192;
+        k_bbox<DB><<<(unsigned)ceil_div(n, chunk), 256, 0, st>>>(coords, n, n_c, rs, n_splits,
+                                                                 chunk, w.bbox);
+        FG_TRY(launched(st));
+    }
+    k_bbox_final<<<(unsigned)ceil_div((int64_t)n_splits * DB, 128), 128, 0, st>>>(
+        w.bbox, rs, n_splits, DB, n_bins, mins, widths);
+    FG_TRY(launched(st));
+    if (n > 0) {
+        k_assign<DB><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
+            coords, n, n_c, rs, n_splits, n_bins, total, mins, widths, bin_idx, w.cursor);
+        FG_TRY(launched(st));
+    }
+    return 0;
+}
+
+}  // namespace binning
+}  // namespace fg
+
+using namespace fg;
+using namespace fg::binning;
+
+extern "C" int fg_bin_workspace_size(int64_t n, int32_t n_splits, int32_t d_bin, int32_t n_bins,
+                                     size_t* bytes) {
+    if (!bytes) return FG_ERR_NULL;
+    if (n < 0 || n_splits < 1 || n_bins < 1) return FG_ERR_BAD_SHAPE;
+    if (d_bin < 1 || d_bin > kMaxBinDims) return FG_ERR_TOO_FEW_DIMS;
+    int64_t total = 1;
+    for (int i = 0; i < d_bin; ++i) total *= n_bins;
+    BinWs w;
+    *bytes = carve(&w, nullptr, n, n_splits, d_bin, total * n_splits);
+    return 0;
+}
+
+extern "C" int fg_bin_by_coordinates(const float* coords, int64_t n, int32_t n_coords,
+                                     const int64_t* row_splits, int32_t n_splits, int32_t d_bin,
+                                     int32_t n_bins, int64_t* bin_idx, int32_t* sort_order,
+                                     int32_t* bin_bounds, double* dim_mins, double* widths,
+                                     float* sorted_coords, void* workspace,
+                                     size_t workspace_bytes, void* stream) {
+    if (n < 0 || n >= ((int64_t)1 << 31) || n_splits < 1 || n_bins < 1) return FG_ERR_BAD_SHAPE;
+    if (n_coords > 16) return FG_ERR_TOO_MANY_DIMS;
+    if (d_bin < 1 || d_bin > kMaxBinDims || d_bin > n_coords) return FG_ERR_TOO_FEW_DIMS;
+    if (!row_splits || !bin_bounds || !dim_mins || !widths || !workspace) return FG_ERR_NULL;
+    if (n > 0 && (!coords || !bin_idx || !sort_order || !sorted_coords)) return FG_ERR_NULL;
+    int64_t total = 1;
+    for (int i = 0; i < d_bin; ++i) total *= n_bins;
+    const int64_t n_cells = total * n_splits;
+    BinWs w;
+    const size_t need = carve(&w, workspace, n, n_splits, d_bin, n_cells);
+    if (workspace_bytes < need) return FG_ERR_WORKSPACE;
+    cudaStream_t st = (cudaStream_t)stream;
+
+    FG_CUDA(cudaMemsetAsync(w.cursor, 0, sizeof(int32_t) * (size_t)n_cells, st));
+    FG_CUDA(cudaMemsetAsync(w.st, 0, sizeof(unsigned long long) * (size_t)w.n_tiles, st));
+    FG_CUDA(cudaMemsetAsync(w.counters, 0, sizeof(unsigned) * 4, st));
+
+    switch (d_bin) {
+        case 1: FG_TRY(launch_bin_core<1>(coords, n, n_coords, row_splits, n_splits, n_bins, total, dim_mins, widths, bin_idx, w, st)); break;
+        case 2: FG_TRY(launch_bin_core<2>(coords, n, n_coords, row_splits, n_splits, n_bins, total, dim_mins, widths, bin_idx, w, st)); break;
+        case 3: FG_TRY(launch_bin_core<3>(coords, n, n_coords, row_splits, n_splits, n_bins, total, dim_mins, widths, bin_idx, w, st)); break;
+        case 4: FG_TRY(launch_bin_core<4>(coords, n, n_coords, row_splits, n_splits, n_bins, total, dim_mins, widths, bin_idx, w, st)); break;
+        default: FG_TRY(launch_bin_core<5>(coords, n, n_coords, row_splits, n_splits, n_bins, total, dim_mins, widths, bin_idx, w, st)); break;
+    }
+    k_scan<<<(unsigned)w.n_tiles, kScanThreads, 0, st>>>(w.cursor, n_cells, bin_bounds, w.cursor,
+                                                        w.st, w.counters);
+    FG_TRY(launched(st));
+    if (n == 0) return 0;
+    k_scatter<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(bin_idx, n, w.cursor, sort_order);
+    FG_TRY(launched(st));
+    const int nv = (n_coords + 3) / 4;
+    switch (nv) {
+        case 1: return launch_fixups<1>(bin_bounds, n_cells, sort_order, bin_idx, row_splits, total, coords, n_coords, sorted_coords, w, st);
+        case 2: return launch_fixups<2>(bin_bounds, n_cells, sort_order, bin_idx, row_splits, total, coords, n_coords, sorted_coords, w, st);
+        case 3: return launch_fixups<3>(bin_bounds, n_cells, sort_order, bin_idx, row_splits, total, coords, n_coords, sorted_coords, w, st);
+        default: return launch_fixups<4>(bin_bounds, n_cells, sort_order, bin_idx, row_splits, total, coords, n_coords, sorted_coords, w, st);
+    }
+}
+
+namespace fg {
+namespace binning {
+__global__ void k_index_replace(int32_t* __restrict__ io, int64_t n, const int32_t* __restrict__ lut) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t x = io[i];
+        if (x >= 0) io[i] = lut[x];
+    }
+}
+}  // namespace binning
+}  // namespace fg
+
+extern "C" int fg_index_replacer(int32_t* io, int64_t n, const int32_t* lut, int64_t lut_n,
+                                 void* stream) {
+    if (n < 0 || lut_n < 0) return FG_ERR_BAD_SHAPE;
+    if (n == 0) return 0;
+    if (!io || !lut) return FG_ERR_NULL;
+    cudaStream_t st = (cudaStream_t)stream;
+    const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(n, 256), 148 * 16);
+    k_index_replace<<<grid, 256, 0, st>>>(io, n, lut);
+    return launched(st);
+}
+
+extern "C" const char* fg_error_string(int code) {
+    switch (code) {
+        case FG_OK: return "ok";
+        case FG_ERR_BAD_K: return "k must be a positive integer within the supported range";
+        case FG_ERR_BAD_SHAPE: return "bad array sizes";
+        case FG_ERR_TOO_FEW_DIMS: return "d_bin must be in [1, 5] and <= n_coords";
+        case FG_ERR_WORKSPACE: return "workspace too small";
+        case FG_ERR_NULL: return "required pointer is NULL";
+        case FG_ERR_TOO_MANY_DIMS: return "n_coords must be <= 16";
+        case FG_ERR_BAD_RADIUS: return "max_radius2 must be >= 0";
+        default: return code > 0 ? cudaGetErrorString((cudaError_t)code) : "unknown error";
+    }
+}
+
+extern "C" int fg_abi_version(void) { return FG_ABI_VERSION; }
+
+extern "C" uint64_t fg_launch_count(void) { return g_launches.load(); }
