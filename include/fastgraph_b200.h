@@ -58,6 +58,7 @@ enum fg_status {
 #define FG_KNN_EXHAUSTIVE 0x4    /* no early stop and no pruning (diagnostic, same result) */
 #define FG_KNN_D2_F64 0x8        /* out_d2 is double (bit-exact reference float64 d2);
                                     otherwise float (= float32 of the reference d2)         */
+#define FG_KNN_STATS 0x100       /* diagnostics: count search events (fg_knn_stats)        */
 
 /* Reducer codes for the GravNet aggregation (G/gravnet.py:26, order = blocks). */
 #define FG_REDUCE_MEAN 0
@@ -107,6 +108,12 @@ int fg_knn_fwd(const float *sorted_coords, const int32_t *sort_order, const int6
                int32_t d_bin, int32_t n_bins, int32_t k, const int8_t *dir_mask,
                double max_radius2, uint32_t flags, int32_t *out_idx, void *out_d2,
                void *stream);
+
+/* Diagnostics: copy (and optionally reset) the counters accumulated by
+ * fg_knn_fwd launches made with FG_KNN_STATS: [queries, regions, chunks,
+ * appends, compactions, speculative-radius failures, exact epilogues, rows].
+ * Synchronous; not for the hot path. */
+int fg_knn_stats(uint64_t *out, int32_t n, int32_t reset);
 
 /* ---------------------------------------------------------------- backward */
 

@@ -20,6 +20,7 @@ FG_KNN_USE_DIRECTION = 0x1
 FG_KNN_USE_MAX_R2 = 0x2
 FG_KNN_EXHAUSTIVE = 0x4
 FG_KNN_D2_F64 = 0x8
+FG_KNN_STATS = 0x100
 FG_REDUCE_MEAN = 0
 FG_REDUCE_MAX = 1
 
@@ -28,7 +29,7 @@ EXPORTS = (
     "fg_bin_workspace_size", "fg_bin_by_coordinates", "fg_index_replacer", "fg_knn_fwd",
     "fg_knn_bwd_workspace_size", "fg_knn_bwd", "fg_gravnet_fwd",
     "fg_gravnet_bwd_workspace_size", "fg_gravnet_bwd", "fg_error_string", "fg_abi_version",
-    "fg_launch_count",
+    "fg_launch_count", "fg_knn_stats",
 )
 
 _P = ctypes.c_void_p
@@ -55,6 +56,7 @@ _SIGS = {
     "fg_error_string": ([ctypes.c_int], ctypes.c_char_p),
     "fg_abi_version": ([], ctypes.c_int),
     "fg_launch_count": ([], ctypes.c_uint64),
+    "fg_knn_stats": ([_P, _I32, _I32], ctypes.c_int),
 }
 
 _lib = None

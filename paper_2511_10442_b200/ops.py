@@ -37,6 +37,22 @@ from . import _lib
 from .errors import BackendUnavailableError, BadShapeError, ShapeMismatchError
 
 _LIB_NS = "fastgraph"
+_DEBUG_FLAGS = 0  # OR-ed into fg_knn_fwd flags (diagnostics only, see set_debug_flags)
+
+
+def set_debug_flags(flags: int) -> None:
+    """Diagnostics: e.g. ``set_debug_flags(_lib.FG_KNN_STATS)`` makes every search
+    launch count its events (read them with ``knn_stats()``)."""
+    global _DEBUG_FLAGS
+    _DEBUG_FLAGS = int(flags)
+
+
+def knn_stats(reset: bool = True) -> dict:
+    names = ("queries", "regions", "chunks", "appends", "compactions", "spec_fail", "exact_epi",
+             "rows")
+    buf = (ctypes.c_uint64 * len(names))()
+    _lib.check(_lib.load().fg_knn_stats(ctypes.cast(buf, ctypes.c_void_p), len(names), int(reset)))
+    return dict(zip(names, [int(x) for x in buf]))
 
 
 def _p(t: Optional[Tensor]):
@@ -147,6 +163,7 @@ def binned_select_knn(coords: Tensor, row_splits: Tensor, bin_idx: Tensor, sort_
         flags |= _lib.FG_KNN_EXHAUSTIVE
     if d2_f64:
         flags |= _lib.FG_KNN_D2_F64
+    flags |= _DEBUG_FLAGS
     idx = torch.empty((n, K), dtype=torch.int32, device=dev)
     d2 = torch.empty((n, K), dtype=torch.float64 if d2_f64 else torch.float32, device=dev)
     _lib.check(L.fg_knn_fwd(_p(sorted_coords), _p(sort_order), _p(bin_idx), _p(bin_bounds), _p(rs),
