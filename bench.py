@@ -40,6 +40,10 @@ C_TOTAL = {"A": 8.6e5, "B": 3.68e9, "north_star": 7.47e8, "C": 1.81e11, "D": 4.5
            "E": 3.31e8}
 
 
+# query sample for the CPU reference where its full search would take minutes+
+REF_QUERY_FRAC = {"C": 0.002, "D": 0.1}
+
+
 def algorithmic_bytes(n, d, k, c_total):
     """B_fwd = 4Nd + 4d*C_total + 8Nk; B_bwd = 8Nk + 8Ndk + 8Nd."""
     b_fwd = 4 * n * d + 4 * d * c_total + 8 * n * k
@@ -137,11 +141,14 @@ def workload(config, rank, world):
     return coords.astype(np.float32), off, k, n_bins, "weak", desc
 
 
-def cpu_reference_sample(coords32, offsets, k, n_bins, sample, seed=0):
-    """The reference's own CPU path (oracle/_ref = its compiled _binned_cy
-    kernels; backward = the oracle's restatement of its numpy knn_backward)
-    timed on a query sample.  Returns (seconds extrapolated to all queries,
-    details dict)."""
+def cpu_reference_step(coords32, offsets, k, n_bins, bwd_rows=100_000, seed=0,
+                       query_frac=1.0):
+    """One step of the reference's own CPU path on this host: build_index +
+    binned_knn over ALL queries (oracle/_ref = the reference's compiled
+    _binned_cy kernels, all host threads) + knn_backward (the oracle's
+    restatement of the reference's numpy np.add.at code, 1 core) on a sample of
+    rows, extrapolated linearly (the backward has no per-call fixed cost).
+    Returns (seconds for the full workload, details)."""
     from oracle import oracle as O  # cpu_baseline leg only
     ref = O.load_ref_kernels()
     kind = "reference" if ref is not None else "port"
@@ -149,39 +156,47 @@ def cpu_reference_sample(coords32, offsets, k, n_bins, sample, seed=0):
     n, n_c = c64.shape
     d_bin = min(n_c, 5)
     threads = os.cpu_count() or 1
-    t0 = time.perf_counter()
-    if ref is not None:
-        bi, so, bb, mins, widths = ref.build_index(c64, offsets, d_bin, n_bins)
-    else:
-        bi, so, bb, mins, widths = O.build_index(c64, offsets, d_bin, n_bins)
-    t_build = time.perf_counter() - t0
     rng = np.random.default_rng(seed)
-    rows = rng.choice(n, size=min(sample, n), replace=False)
-    mask = np.zeros(n, np.int8)      # role 0: candidate only
-    mask[rows] = 3                   # sampled rows run their query
-    out_i = np.empty((n, k), np.int32)
-    out_d = np.empty((n, k), np.float64)
-    bc = np.full(d_bin, n_bins, np.int64)
-    t0 = time.perf_counter()
-    if ref is not None:
-        ref.binned_knn(c64, bi, so, bb, bc, widths.min(axis=1).copy(), mask, True, 0.0, False,
-                       False, k, out_i, out_d, threads)
-    else:
-        O.lib().orc_binned_knn_refslot  # noqa: B018
-        oi, od = O.knn_refslot(c64, offsets, k, dir_mask=mask, n_bins=n_bins, threads=threads)
-    t_search = time.perf_counter() - t0
+    mask = None
+    if query_frac < 1.0:  # configs whose full CPU search takes hours (C): query sample
+        mask = np.zeros(n, np.int8)  # role 0: candidate only
+        mask[rng.choice(n, size=max(1, int(n * query_frac)), replace=False)] = 3
+
+    def run(m):
+        t0 = time.perf_counter()
+        if ref is not None:
+            bi, so, bb, mins, widths = ref.build_index(c64, offsets, d_bin, n_bins)
+            oi = np.empty((n, k), np.int32)
+            od = np.empty((n, k), np.float64)
+            ref.binned_knn(c64, bi, so, bb, np.full(d_bin, n_bins, np.int64),
+                           widths.min(axis=1).copy(), np.zeros(1, np.int8) if m is None else m,
+                           m is not None, 0.0, False, False, k, oi, od, threads)
+        else:
+            oi, od = O.knn_refslot(c64, offsets, k, n_bins=n_bins, dir_mask=m, threads=threads)
+        return time.perf_counter() - t0, oi
+
+    if mask is None:
+        t_fwd, out_i = run(None)
+    else:  # fixed per-vertex cost measured with zero queries, query cost scaled
+        t_zero, _ = run(np.zeros(n, np.int8))
+        t_s, out_i = run(mask)
+        t_fwd = t_zero + max(t_s - t_zero, 0.0) / query_frac
+        sel = np.nonzero(mask == 3)[0]
+        out_i = out_i.copy()
+        out_i[np.setdiff1d(np.arange(n), sel)] = out_i[sel[0]]  # bwd rows use real neighbours
+    rows = rng.choice(n, size=min(bwd_rows, n), replace=False)
     up = rng.standard_normal((len(rows), k))
     t0 = time.perf_counter()
     O.knn_backward_numpy(c64, out_i[rows], up, rows)
-    t_bwd = time.perf_counter() - t0
-    scale = n / len(rows)
-    total = t_build + (t_search + t_bwd) * scale
-    return total, {"kind": kind, "cores": threads, "t_build_s": t_build,
-                   "t_search_sample_s": t_search, "t_bwd_sample_s": t_bwd,
-                   "sample": (f"{len(rows)} of {n} queries (DirectionMask roles 3/0), search "
-                              f"x{scale:.0f} + full build_index; fwd = reference compiled "
-                              f"_binned_cy on {threads} threads, bwd = numpy knn_backward "
-                              "restatement (1 core)")}
+    t_bwd = (time.perf_counter() - t0) * (n / len(rows))
+    total = t_fwd + t_bwd
+    return total, {"kind": kind, "cores": threads, "t_fwd_s": t_fwd, "t_bwd_s": t_bwd,
+                   "sample": (f"fwd: build_index + binned_knn over "
+                              + (f"all {n} queries" if mask is None else
+                                 f"a {query_frac:.0%} query sample (fixed per-vertex cost timed "
+                                 f"separately, query cost x{1 / query_frac:.0f})")
+                              + f" (reference compiled _binned_cy, {threads} threads); bwd: numpy "
+                              f"knn_backward on {len(rows)} rows x{n / len(rows):.0f} (1 core)")}
 
 
 def run_reference(args):
@@ -190,14 +205,13 @@ def run_reference(args):
         return 0
     coords, off, k, n_bins, scaling, desc = workload(args.config, 0, 1)
     n = coords.shape[0]
-    sample = args.ref_sample
-    for _ in range(max(args.warmup, 0)):
-        cpu_reference_sample(coords, off, k, n_bins, max(sample // 10, 100), seed=1)
     times = []
     det = None
-    for s in range(args.steps):
-        tt, det = cpu_reference_sample(coords, off, k, n_bins, sample, seed=100 + s)
-        times.append(tt)
+    for s_ in range(max(args.warmup, 0) + args.steps):
+        tt, det = cpu_reference_step(coords, off, k, n_bins, seed=100 + s_,
+                                     query_frac=REF_QUERY_FRAC.get(args.config, 1.0))
+        if s_ >= args.warmup:
+            times.append(tt)
     t = float(np.mean(times))
     value = n / t
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s",
@@ -220,7 +234,6 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="north_star", choices=["north_star", "A", "B", "C", "D", "E"])
-    ap.add_argument("--ref-sample", type=int, default=10_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
@@ -375,7 +388,8 @@ def main():
                        "ms_per_step": e2e_ms}
     if world == 1 and not args.no_cpu_baseline:
         try:
-            tt, det = cpu_reference_sample(coords_np, off_np, k, n_bins, args.ref_sample)
+            tt, det = cpu_reference_step(coords_np, off_np, k, n_bins,
+                                         query_frac=REF_QUERY_FRAC.get(args.config, 1.0))
             line["cpu_baseline"] = {"value": n / tt, "unit": "queries/s", "cores": det["cores"],
                                     "kind": det["kind"], "sample": det["sample"]}
         except Exception as exc:  # the baseline must not kill the GPU number

@@ -54,7 +54,7 @@ constexpr int kWarpsPerBlock = 4;
 constexpr float kMargin = 1.0f + 1e-5f;
 constexpr float kTiny = 1e-35f;
 constexpr float kCellSlack = 1e-4f;  // cell units
-constexpr float kAlpha = 1.10f;      // speculative radius inflation
+constexpr float kAlpha = 1.07f;      // speculative radius inflation
 constexpr float kInf = __builtin_huge_valf();
 
 enum { ST_QUERIES, ST_REGIONS, ST_CHUNKS, ST_APPENDS, ST_COMPACT, ST_SPEC_FAIL, ST_EXACT_EPI,
@@ -357,7 +357,7 @@ struct Filter {
 
 // Evaluate one group of spans (one per lane: start S, length L) and append
 // the passing candidates.
-template <int NV, int DB, int CAP>
+template <int NV, int DB, int CAP, bool FILT>
 __device__ __forceinline__ void scan_spans(const KnnArgs& a, WarpBuf<CAP>& b,
                                            const Query<NV, DB>& Q, int32_t S, int32_t L, int& m,
                                            int need, float& tau, const Filter& flt, Counters& cnt) {
@@ -394,11 +394,11 @@ __device__ __forceinline__ void scan_spans(const KnnArgs& a, WarpBuf<CAP>& b,
             d2 = fp32_d2<NV>(Q.q, a.sc + (int64_t)cpos * NV);
             pass = d2 <= tau && cpos != Q.p;
         }
-        if (flt.use_dir && pass) {
+        if (FILT && flt.use_dir && pass) {
             const int8_t role = a.dir[a.sid[cpos]];
             pass = role == 0 || role == 3;
         }
-        if (flt.use_r2 && pass) {
+        if (FILT && flt.use_r2 && pass) {
             if (d2 > flt.r2_hi)
                 pass = false;
             else if (d2 >= flt.r2_lo)
@@ -424,7 +424,7 @@ __device__ __forceinline__ void scan_spans(const KnnArgs& a, WarpBuf<CAP>& b,
 }
 
 // Scan region (R_old, R_new]; R_old = -1 means the whole cube(R_new).
-template <int NV, int DB, int CAP>
+template <int NV, int DB, int CAP, bool FILT>
 __device__ void scan_region(const KnnArgs& a, WarpBuf<CAP>& b, const Query<NV, DB>& Q, int R_old,
                             int R_new, bool prune, int& m, int need, float& tau, const Filter& flt,
                             Counters& cnt) {
@@ -487,9 +487,19 @@ __device__ void scan_region(const KnnArgs& a, WarpBuf<CAP>& b, const Query<NV, D
                 L1 = a.bounds[rowcell + b1 + 1] - S1;
             }
         }
-        scan_spans<NV, DB, CAP>(a, b, Q, S0, L0, m, need, tau, flt, cnt);
-        if (R_old >= 0) scan_spans<NV, DB, CAP>(a, b, Q, S1, L1, m, need, tau, flt, cnt);
+        scan_spans<NV, DB, CAP, FILT>(a, b, Q, S0, L0, m, need, tau, flt, cnt);
+        if (R_old >= 0) scan_spans<NV, DB, CAP, FILT>(a, b, Q, S1, L1, m, need, tau, flt, cnt);
     }
+}
+
+template <int NV, int DB, int CAP>
+__device__ __forceinline__ void scan(const KnnArgs& a, WarpBuf<CAP>& b, const Query<NV, DB>& Q,
+                                     int R_old, int R_new, bool prune, int& m, int need, float& tau,
+                                     const Filter& flt, Counters& cnt) {
+    if (flt.use_dir || flt.use_r2)
+        scan_region<NV, DB, CAP, true>(a, b, Q, R_old, R_new, prune, m, need, tau, flt, cnt);
+    else
+        scan_region<NV, DB, CAP, false>(a, b, Q, R_old, R_new, prune, m, need, tau, flt, cnt);
 }
 
 // ---------------------------------------------------------------- epilogue
@@ -658,14 +668,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) k_knn_fwd(KnnArgs a) {
         int m = 0;
         int R_done = -1;
         if (exhaustive) {
-            scan_region<NV, DB, CAP>(a, buf, Q, -1, R_grid, false, m, need, tau, flt, cnt);
+            scan<NV, DB, CAP>(a, buf, Q, -1, R_grid, false, m, need, tau, flt, cnt);
         } else {
             bool plain = true;
             const float tau0 = a.n_c == DB ? density_tau(a, Q, need) : kInf;
             if (tau0 < tau) {
                 const int R0 = cover_radius(Q, nb, tau0);
                 float t0 = tau0;
-                scan_region<NV, DB, CAP>(a, buf, Q, -1, R0, true, m, need, t0, flt, cnt);
+                scan<NV, DB, CAP>(a, buf, Q, -1, R0, true, m, need, t0, flt, cnt);
                 // certified iff >= need entries lie strictly inside tau0
                 const float inner = tau0 * (1.0f - 3e-5f);
                 int c_in = 0;
@@ -690,7 +700,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) k_knn_fwd(KnnArgs a) {
             }
             while (R_next > R_done) {
                 const bool prune = tau < kInf;
-                scan_region<NV, DB, CAP>(a, buf, Q, R_done, R_next, prune, m, need, tau, flt, cnt);
+                scan<NV, DB, CAP>(a, buf, Q, R_done, R_next, prune, m, need, tau, flt, cnt);
                 R_done = R_next;
                 if (R_done >= R_grid) break;
                 if (m >= need) m = compact<NV, CAP>(a, buf, m, need, tau, Q.q, cnt);
@@ -698,11 +708,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) k_knn_fwd(KnnArgs a) {
             }
         }
         bool done = false;
-        if (m > 128) m = compact<NV, CAP>(a, buf, m, need, tau, Q.q, cnt);
-        if (m <= 64 && need <= 63)
-            done = epilogue_fast<NV, 2, CAP>(a, buf, Q.q, m, need, row_out);
-        else if (m <= 128 && need <= 127)
-            done = epilogue_fast<NV, 4, CAP>(a, buf, Q.q, m, need, row_out);
+        if (m > 64 && need <= 63) m = compact<NV, CAP>(a, buf, m, need, tau, Q.q, cnt);
+        if (m <= 64 && need <= 63) done = epilogue_fast<NV, 2, CAP>(a, buf, Q.q, m, need, row_out);
         if (!done) {
             ++cnt.exact;
             epilogue_exact<NV, CAP>(a, buf, Q.q, m, k, row_out);
@@ -734,7 +741,8 @@ int launch_knn(const KnnArgs& a, cudaStream_t st) {
 
 template <int NV, int DB>
 int dispatch_cap(const KnnArgs& a, cudaStream_t st) {
-    if (a.k - 1 + 64 <= 128) return launch_knn<NV, DB, 128>(a, st);
+    const int need = a.k - 1;
+    if (need + 64 <= 128) return launch_knn<NV, DB, 128>(a, st);
     return launch_knn<NV, DB, 1024>(a, st);
 }
 
