@@ -275,11 +275,17 @@ def main():
                                         None, None, False, False)
         ev_bwd = torch.cuda.Event(enable_timing=True)
         ev_bwd.record(stream)
-        g = ops.binned_select_knn_grad(u, idx, c)
+        g = ops.binned_select_knn_grad(u, idx, c, so)
         return idx, d2, g, ev_knn, ev_bwd
 
-    for _ in range(max(args.warmup, 3) if args.warmup > 0 else 0):
+    # warm-up: at least W steps and at least 1.5 s of work, so the SM clocks have
+    # left their idle state before anything is timed
+    t_warm = time.perf_counter()
+    it = 0
+    while it < max(args.warmup, 3) or time.perf_counter() - t_warm < 1.5:
         step(coords, up)
+        torch.cuda.synchronize()
+        it += 1
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()

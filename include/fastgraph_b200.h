@@ -122,11 +122,13 @@ int fg_knn_bwd_workspace_size(int64_t n, int32_t n_coords, size_t *bytes);
 /* binned_select_knn backward.  Replaces knn_backward (G/knn.py:135-168):
  * for every valid non-self slot (v,s) -> u with upstream g = grad_d2[v,s],
  * grad[v] += 2g(x_v - x_u) and grad[u] -= 2g(x_v - x_u).  Terms are formed
- * exactly in float64 and accumulated in float64; grad_coords is float32
- * (or double with grad_is_f64). */
+ * exactly in float64 and accumulated to float64-class precision (compensated
+ * fp32x4 atomics, error ~2^-48 of the term magnitudes); grad_coords is float32
+ * (or double with grad_is_f64).  `order` (nullable) is the row visiting order,
+ * e.g. the sort_order of fg_bin_by_coordinates (spatial locality). */
 int fg_knn_bwd(const float *coords, int64_t n, int32_t n_coords, const int32_t *idx, int32_t k,
-               const float *grad_d2, void *grad_coords, int32_t grad_is_f64, void *workspace,
-               size_t workspace_bytes, void *stream);
+               const float *grad_d2, const int32_t *order, void *grad_coords, int32_t grad_is_f64,
+               void *workspace, size_t workspace_bytes, void *stream);
 
 /* ---------------------------------------------------------------- GravNet */
 

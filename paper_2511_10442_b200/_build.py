@@ -41,17 +41,20 @@ def needs_rebuild() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_rebuild():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """Compile csrc/*.cu; ``defines``/``out`` build an experimental variant."""
+    target = out or LIB_PATH
+    if not force and not defines and out is None and not needs_rebuild():
         return LIB_PATH
     objs = []
-    tmp = os.path.join(PKG, "build")
+    tmp = os.path.join(PKG, "build" if not defines else "build_" + "_".join(d.replace("=", "") for d in defines))
     os.makedirs(tmp, exist_ok=True)
     procs = []
     for src in sources():
         obj = os.path.join(tmp, os.path.basename(src).replace(".cu", ".o"))
         cmd = [nvcc(), ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                *(["-Xptxas", "-v"] if verbose else []),
+               *["-D" + d for d in defines],
                "-I" + os.path.join(ROOT, "include"), "-c", src, "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
                                             text=True)))
@@ -64,10 +67,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
         failed |= p.returncode != 0
     if failed:
         raise RuntimeError("nvcc failed")
-    tmp_lib = LIB_PATH + ".tmp"
+    tmp_lib = target + ".tmp"
     subprocess.run([nvcc(), ARCH, "-shared", "-o", tmp_lib, *objs], check=True)
-    os.replace(tmp_lib, LIB_PATH)
-    return LIB_PATH
+    os.replace(tmp_lib, target)
+    return target
 
 
 if __name__ == "__main__":

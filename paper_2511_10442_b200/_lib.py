@@ -14,7 +14,8 @@ from .errors import (BackendUnavailableError, BadKError, BadShapeError, GridKnnE
                      ShapeMismatchError, TooFewDimsError)
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libfastgraph_b200.so")
+# FG_LIB_PATH selects an experimental build of the same ABI (benchmarking only)
+LIB_PATH = os.environ.get("FG_LIB_PATH") or os.path.join(PKG, "libfastgraph_b200.so")
 
 FG_KNN_USE_DIRECTION = 0x1
 FG_KNN_USE_MAX_R2 = 0x2
@@ -47,7 +48,7 @@ _SIGS = {
     "fg_knn_fwd": ([_P, _P, _P, _P, _P, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _P, _D, _U32,
                     _P, _P, _P], ctypes.c_int),
     "fg_knn_bwd_workspace_size": ([_I64, _I32, _SZ], ctypes.c_int),
-    "fg_knn_bwd": ([_P, _I64, _I32, _P, _I32, _P, _P, _I32, _P, ctypes.c_size_t, _P],
+    "fg_knn_bwd": ([_P, _I64, _I32, _P, _I32, _P, _P, _P, _I32, _P, ctypes.c_size_t, _P],
                    ctypes.c_int),
     "fg_gravnet_fwd": ([_P, _I64, _I32, _P, _P, _I32, _D, _P, _I32, _I32, _P, _P], ctypes.c_int),
     "fg_gravnet_bwd_workspace_size": ([_I64, _I32, _SZ], ctypes.c_int),

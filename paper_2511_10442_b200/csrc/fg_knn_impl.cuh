@@ -45,6 +45,13 @@
 #pragma once
 #include <cfloat>
 
+#ifndef FG_SPAN_WALK
+#define FG_SPAN_WALK 0
+#endif
+#ifndef FG_KNN_MINB
+#define FG_KNN_MINB 8
+#endif
+
 #include "fg_common.cuh"
 
 namespace fg {
@@ -167,7 +174,7 @@ __device__ void warp_sort_exact(WarpBuf<CAP>& b, int len) {
 // Exact keys for buffer entries [0, m) (beyond-radius entries get the
 // sentinel), sorted by (d2_f64, original index).
 template <int NV, int CAP>
-__device__ void exact_keys_and_sort(const KnnArgs& a, WarpBuf<CAP>& b, int m,
+__device__ __noinline__ void exact_keys_and_sort(const KnnArgs& a, WarpBuf<CAP>& b, int m,
                                     const float (&q)[4 * NV]) {
     const int lane = lane_id();
     int len = 32;
@@ -198,7 +205,7 @@ __device__ void exact_keys_and_sort(const KnnArgs& a, WarpBuf<CAP>& b, int m,
 // ties) keep exactly the `need` best by exact key.  Returns the new count and
 // tightens tau.
 template <int NV, int CAP>
-__device__ int compact(const KnnArgs& a, WarpBuf<CAP>& b, int m, int need, float& tau,
+__device__ __noinline__ int compact(const KnnArgs& a, WarpBuf<CAP>& b, int m, int need, float& tau,
                        const float (&q)[4 * NV], Counters& cnt) {
     const int lane = lane_id();
     ++cnt.compacts;
@@ -364,6 +371,51 @@ __device__ __forceinline__ void scan_spans(const KnnArgs& a, WarpBuf<CAP>& b,
     const int lane = lane_id();
     const unsigned nonempty = __ballot_sync(FG_FULL_MASK, L > 0);
     if (!nonempty) return;
+    // Short spans (uniform data: a trimmed row holds a few points): every lane
+    // walks its own span; the warp runs max(L) steps with no flattening.  Long
+    // spans (clusters): flatten into full 32-candidate chunks below.
+    const int max_len = __reduce_max_sync(FG_FULL_MASK, (unsigned)L);
+    const int total = __reduce_add_sync(FG_FULL_MASK, (unsigned)L);
+    if (FG_SPAN_WALK && max_len * 2 <= ((total + 31) >> 5) * 5) {
+        for (int i = 0; i < max_len; ++i) {
+            ++cnt.chunks;
+            const bool live = i < L;
+            const int32_t cpos = S + i;
+            bool pass = false;
+            float d2 = kInf;
+            if (live) {
+                d2 = fp32_d2<NV>(Q.q, a.sc + (int64_t)cpos * NV);
+                pass = d2 <= tau && cpos != Q.p;
+            }
+            if (FILT && flt.use_dir && pass) {
+                const int8_t role = a.dir[a.sid[cpos]];
+                pass = role == 0 || role == 3;
+            }
+            if (FILT && flt.use_r2 && pass) {
+                if (d2 > flt.r2_hi)
+                    pass = false;
+                else if (d2 >= flt.r2_lo)
+                    pass = exact_pos_d2<NV>(a, Q.q, cpos) <= a.max_r2;
+            }
+            unsigned bal = __ballot_sync(FG_FULL_MASK, pass);
+            if (bal) {
+                if (m + __popc(bal) > CAP) {
+                    m = compact<NV, CAP>(a, b, m, need, tau, Q.q, cnt);
+                    pass = pass && d2 <= tau;
+                    bal = __ballot_sync(FG_FULL_MASK, pass);
+                }
+                if (pass) {
+                    const int pos = m + __popc(bal & lanemask_lt());
+                    b.d[pos] = d2;
+                    b.p[pos] = cpos;
+                }
+                m += __popc(bal);
+                cnt.appends += __popc(bal);
+                __syncwarp();
+            }
+        }
+        return;
+    }
     const int ns = __popc(nonempty);
     if (L > 0) {
         const int dst = __popc(nonempty & lanemask_lt());
@@ -503,97 +555,72 @@ __device__ __forceinline__ void scan(const KnnArgs& a, WarpBuf<CAP>& b, const Qu
 }
 
 // ---------------------------------------------------------------- epilogue
-// Fast path for m <= 32*E: sort (float32(d2_f64) bits, position) in registers,
-// E keys per lane at index E*lane + t.  Returns false when entries that decide
-// the row share a float32 value (the exact path then runs).
-template <int NV, int E, int CAP>
+// Fast path for m <= 64: key = float32(d2_f64) bits (monotone for d2 >= 0),
+// lane l owns entries l and l+32; every entry's output slot is its rank, i.e.
+// the number of entries with a smaller key (counted against keys broadcast
+// from shared memory).  If two valid entries share a key and one of them
+// lands in the row (rank < need), the float32 keys cannot decide the order
+// (exact ties / sub-ulp near-ties): returns false and the exact path runs.
+template <int NV, int CAP>
 __device__ bool epilogue_fast(const KnnArgs& a, WarpBuf<CAP>& b, const float (&q)[4 * NV], int m,
                               int need, int64_t row_out) {
-    constexpr int N = 32 * E;
     const int lane = lane_id();
     const bool use_r2 = a.flags & FG_KNN_USE_MAX_R2;
-    unsigned kx[E];  // float32(d2_f64) bits (monotone for d2 >= 0); invalid = ~0
-    int32_t px[E];   // sorted position
+    unsigned key[2];
+    int32_t pos[2];
 #pragma unroll
-    for (int t = 0; t < E; ++t) {
-        const int e = E * lane + t;
-        kx[t] = ~0u;
-        px[t] = -1;
+    for (int t = 0; t < 2; ++t) {
+        const int e = lane + 32 * t;
+        key[t] = ~0u;
+        pos[t] = -1;
         if (e < m) {
-            const int32_t cpos = b.p[e];
-            const double d = exact_pos_d2<NV>(a, q, cpos);
-            if (!use_r2 || d <= a.max_r2) {
-                kx[t] = __float_as_uint(__double2float_rn(d));
-                px[t] = cpos;
-            }
+            pos[t] = b.p[e];
+            const double d = exact_pos_d2<NV>(a, q, pos[t]);
+            if (!use_r2 || d <= a.max_r2) key[t] = __float_as_uint(__double2float_rn(d));
         }
     }
+    unsigned* kb = reinterpret_cast<unsigned*>(b.key);  // reuse as a 32-bit key array
+    __syncwarp();
+    kb[lane] = key[0];
+    kb[lane + 32] = key[1];
+    __syncwarp();
+    int rank[2] = {0, 0}, same[2] = {0, 0};
+    for (int j = 0; j < m; ++j) {
+        const unsigned kj = kb[j];
 #pragma unroll
-    for (int k2 = 2; k2 <= N; k2 <<= 1) {
-#pragma unroll
-        for (int j2 = k2 >> 1; j2 > 0; j2 >>= 1) {
-            if (j2 < E) {
-#pragma unroll
-                for (int t = 0; t < E; ++t) {
-                    if ((t & j2) == 0) {
-                        const int u = t | j2;
-                        const bool asc = ((E * lane + t) & k2) == 0;
-                        const bool sw = asc ? (kx[t] > kx[u]) : (kx[t] < kx[u]);
-                        const unsigned k0 = sw ? kx[u] : kx[t], k1 = sw ? kx[t] : kx[u];
-                        const int32_t p0 = sw ? px[u] : px[t], p1 = sw ? px[t] : px[u];
-                        kx[t] = k0; kx[u] = k1; px[t] = p0; px[u] = p1;
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int t = 0; t < E; ++t) {
-                    const int i = E * lane + t;
-                    const unsigned ok = __shfl_xor_sync(FG_FULL_MASK, kx[t], j2 / E);
-                    const int32_t op = __shfl_xor_sync(FG_FULL_MASK, px[t], j2 / E);
-                    const bool keep_min = ((i & j2) == 0) == ((i & k2) == 0);
-                    const bool take = keep_min ? (ok < kx[t]) : (ok > kx[t]);
-                    kx[t] = take ? ok : kx[t];
-                    px[t] = take ? op : px[t];
-                }
-            }
+        for (int t = 0; t < 2; ++t) {
+            rank[t] += kj < key[t] ? 1 : 0;
+            same[t] += kj == key[t] ? 1 : 0;
         }
     }
-    // entries that decide the row: pairs (i, i+1) with i + 1 <= need
     bool amb = false;
 #pragma unroll
-    for (int t = 0; t + 1 < E; ++t) {
-        const int i = E * lane + t;
-        amb |= i + 1 <= need && kx[t + 1] != ~0u && kx[t] == kx[t + 1];
-    }
-    {
-        const unsigned nxt = __shfl_down_sync(FG_FULL_MASK, kx[0], 1);
-        const int i = E * lane + E - 1;
-        amb |= lane < 31 && i + 1 <= need && nxt != ~0u && kx[E - 1] == nxt;
-    }
+    for (int t = 0; t < 2; ++t) amb |= key[t] != ~0u && same[t] > 1 && rank[t] < need;
     if (__any_sync(FG_FULL_MASK, amb)) return false;
     const bool f64 = a.flags & FG_KNN_D2_F64;
+    int valid = 0;
 #pragma unroll
-    for (int t = 0; t < E; ++t) {
-        const int i = E * lane + t;
-        if (i < need) {
-            const int64_t off = row_out + 1 + i;
-            if (kx[t] != ~0u) {
-                a.out_idx[off] = a.sid[px[t]];
-                if (f64)
-                    reinterpret_cast<double*>(a.out_d2)[off] = exact_pos_d2<NV>(a, q, px[t]);
-                else
-                    reinterpret_cast<float*>(a.out_d2)[off] = __uint_as_float(kx[t]);
-            } else {
-                a.out_idx[off] = -1;
-                store_d2(a, off, 0.0);
-            }
+    for (int t = 0; t < 2; ++t) {
+        valid += key[t] != ~0u ? 1 : 0;
+        if (key[t] != ~0u && rank[t] < need) {
+            const int64_t off = row_out + 1 + rank[t];
+            a.out_idx[off] = a.sid[pos[t]];
+            if (f64)
+                reinterpret_cast<double*>(a.out_d2)[off] = exact_pos_d2<NV>(a, q, pos[t]);
+            else
+                reinterpret_cast<float*>(a.out_d2)[off] = __uint_as_float(key[t]);
         }
+    }
+    valid = __reduce_add_sync(FG_FULL_MASK, valid);
+    for (int sl = valid + lane; sl < need; sl += 32) {  // padding
+        a.out_idx[row_out + 1 + sl] = -1;
+        store_d2(a, row_out + 1 + sl, 0.0);
     }
     return true;
 }
 
 template <int NV, int CAP>
-__device__ void epilogue_exact(const KnnArgs& a, WarpBuf<CAP>& b, const float (&q)[4 * NV], int m,
+__device__ __noinline__ void epilogue_exact(const KnnArgs& a, WarpBuf<CAP>& b, const float (&q)[4 * NV], int m,
                                int k, int64_t row_out) {
     const int lane = lane_id();
     exact_keys_and_sort<NV, CAP>(a, b, m, q);
@@ -610,113 +637,102 @@ __device__ void epilogue_exact(const KnnArgs& a, WarpBuf<CAP>& b, const float (&
     }
 }
 
-// ---------------------------------------------------------------- kernel
-template <int NV, int DB, int CAP>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) k_knn_fwd(KnnArgs a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    WarpBuf<CAP>& buf = reinterpret_cast<WarpBuf<CAP>*>(smem_raw)[threadIdx.x >> 5];
-    const int lane = lane_id();
-    const int64_t warp_global = blockIdx.x * (int64_t)kWarpsPerBlock + (threadIdx.x >> 5);
-    const int64_t warps_total = (int64_t)gridDim.x * kWarpsPerBlock;
-    const int k = a.k, need = k - 1;
+// ---------------------------------------------------------------- per-query pieces
+template <int NV, int DB>
+__device__ __forceinline__ void setup_query(const KnnArgs& a, int64_t p, Query<NV, DB>& Q) {
     const int nb = a.nb;
+    Q.p = (int32_t)p;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        const float4 x = a.sc[p * NV + j];
+        Q.q[4 * j] = x.x; Q.q[4 * j + 1] = x.y; Q.q[4 * j + 2] = x.z; Q.q[4 * j + 3] = x.w;
+    }
+    const int s = a.n_splits == 1 ? 0 : split_of(a.rs, a.n_splits, p);
+    Q.cell_base = (int64_t)s * a.total;
+#pragma unroll
+    for (int i = 0; i < DB; ++i) {
+        const float mn = (float)a.mins[(int64_t)s * DB + i];  // a float32 value
+        Q.w[i] = (float)a.widths[(int64_t)s * DB + i];
+        Q.invw[i] = __frcp_rn(Q.w[i]);
+        Q.qc[i] = (Q.q[i] - mn) * Q.invw[i];
+        Q.c[i] = min(max(__float2int_rd(Q.qc[i]), 0), nb - 1);
+    }
+}
+
+// Self slot; padding of a row that runs no query.  Returns true when the
+// query is skipped (k == 1, or its role is 0/2).
+__device__ __forceinline__ bool begin_row(const KnnArgs& a, int32_t qid, int64_t row_out, int need,
+                                          const Filter& flt) {
+    const int lane = lane_id();
+    if (lane == 0) {
+        a.out_idx[row_out] = qid;
+        store_d2(a, row_out, 0.0);
+    }
+    const bool skip = need == 0 || (flt.use_dir && (a.dir[qid] == 0 || a.dir[qid] == 2));
+    if (skip) {
+        for (int s = 1 + lane; s < a.k; s += 32) {
+            a.out_idx[row_out + s] = -1;
+            store_d2(a, row_out + s, 0.0);
+        }
+    }
+    return skip;
+}
+
+// Plain growth from the query's own cell (or its 3^d cube): regions until the
+// cover radius of tau is scanned.  Fills buf, returns the count, sets tau.
+template <int NV, int DB, int CAP>
+__device__ __noinline__ int plain_search(const KnnArgs& a, WarpBuf<CAP>& buf, const Query<NV, DB>& Q,
+                            int32_t qid, int need, const Filter& flt, float& tau, Counters& cnt) {
+    const int nb = a.nb;
+    const int R_grid = grid_radius(Q, nb);
+    int m = 0, R_done = -1;
+    const int64_t own = a.bin_idx[qid];
+    const int own_cnt = a.bounds[own + 1] - a.bounds[own];
+    int R_next = own_cnt > need ? 0 : min(1, R_grid);
+    while (R_next > R_done) {
+        scan<NV, DB, CAP>(a, buf, Q, R_done, R_next, tau < kInf, m, need, tau, flt, cnt);
+        R_done = R_next;
+        if (R_done >= R_grid) break;
+        if (m >= need) m = compact<NV, CAP>(a, buf, m, need, tau, Q.q, cnt);
+        R_next = tau < kInf ? cover_radius(Q, nb, tau) : R_done + 1;
+    }
+    return m;
+}
+
+// >= need buffered entries strictly inside tau0 (3e-5 margin): certified.
+template <int CAP>
+__device__ __forceinline__ bool certified(const WarpBuf<CAP>& buf, int m, int need, float tau0) {
+    const float inner = tau0 * (1.0f - 3e-5f);
+    int c_in = 0;
+    for (int e = lane_id(); e < m; e += 32) c_in += buf.d[e] <= inner ? 1 : 0;
+    return __reduce_add_sync(FG_FULL_MASK, c_in) >= need;
+}
+
+template <int NV, int CAP>
+__device__ __forceinline__ void finish_query(const KnnArgs& a, WarpBuf<CAP>& buf,
+                                             const float (&q)[4 * NV], int m, int need, float tau,
+                                             int64_t row_out, Counters& cnt) {
+    bool done = false;
+    if (m > 64 && need <= 63) m = compact<NV, CAP>(a, buf, m, need, tau, q, cnt);
+    if (m <= 64 && need <= 63) done = epilogue_fast<NV, CAP>(a, buf, q, m, need, row_out);
+    if (!done) {
+        ++cnt.exact;
+        epilogue_exact<NV, CAP>(a, buf, q, m, a.k, row_out);
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ Filter make_filter(const KnnArgs& a) {
     Filter flt;
     flt.use_dir = a.flags & FG_KNN_USE_DIRECTION;
     flt.use_r2 = a.flags & FG_KNN_USE_MAX_R2;
     flt.r2_hi = flt.use_r2 ? (float)(a.max_r2 * (1.0 + 1e-5)) + kTiny : 0.0f;
     flt.r2_lo = flt.use_r2 ? (float)(a.max_r2 * (1.0 - 1e-5)) : 0.0f;
-    const float r2_tau = flt.use_r2 ? flt.r2_hi : kInf;
-    const bool exhaustive = a.flags & FG_KNN_EXHAUSTIVE;
-    Counters cnt;
-    int64_t queries = 0;
+    return flt;
+}
 
-    for (int64_t p = warp_global; p < a.n; p += warps_total) {
-        ++queries;
-        const int32_t qid = a.sid[p];
-        const int64_t row_out = (int64_t)qid * k;
-        if (lane == 0) {
-            a.out_idx[row_out] = qid;
-            store_d2(a, row_out, 0.0);
-        }
-        const bool skip = need == 0 || (flt.use_dir && (a.dir[qid] == 0 || a.dir[qid] == 2));
-        if (skip) {
-            for (int s = 1 + lane; s < k; s += 32) {
-                a.out_idx[row_out + s] = -1;
-                store_d2(a, row_out + s, 0.0);
-            }
-            continue;
-        }
-        Query<NV, DB> Q;
-        Q.p = (int32_t)p;
-#pragma unroll
-        for (int j = 0; j < NV; ++j) {
-            const float4 x = a.sc[p * NV + j];
-            Q.q[4 * j] = x.x; Q.q[4 * j + 1] = x.y; Q.q[4 * j + 2] = x.z; Q.q[4 * j + 3] = x.w;
-        }
-        const int s = a.n_splits == 1 ? 0 : split_of(a.rs, a.n_splits, p);
-        Q.cell_base = (int64_t)s * a.total;
-#pragma unroll
-        for (int i = 0; i < DB; ++i) {
-            const float mn = (float)a.mins[(int64_t)s * DB + i];  // a float32 value
-            Q.w[i] = (float)a.widths[(int64_t)s * DB + i];
-            Q.invw[i] = __frcp_rn(Q.w[i]);
-            Q.qc[i] = (Q.q[i] - mn) * Q.invw[i];
-            Q.c[i] = min(max(__float2int_rd(Q.qc[i]), 0), nb - 1);
-        }
-        const int R_grid = grid_radius(Q, nb);
-        float tau = r2_tau;
-        int m = 0;
-        int R_done = -1;
-        if (exhaustive) {
-            scan<NV, DB, CAP>(a, buf, Q, -1, R_grid, false, m, need, tau, flt, cnt);
-        } else {
-            bool plain = true;
-            const float tau0 = a.n_c == DB ? density_tau(a, Q, need) : kInf;
-            if (tau0 < tau) {
-                const int R0 = cover_radius(Q, nb, tau0);
-                float t0 = tau0;
-                scan<NV, DB, CAP>(a, buf, Q, -1, R0, true, m, need, t0, flt, cnt);
-                // certified iff >= need entries lie strictly inside tau0
-                const float inner = tau0 * (1.0f - 3e-5f);
-                int c_in = 0;
-                for (int e = lane; e < m; e += 32) c_in += buf.d[e] <= inner ? 1 : 0;
-                c_in = __reduce_add_sync(FG_FULL_MASK, c_in);
-                if (c_in >= need) {
-                    tau = t0;
-                    R_done = R0;
-                    plain = false;
-                } else {
-                    ++cnt.spec_fail;
-                    m = 0;  // tau0 was too small: rescan without it
-                }
-            }
-            int R_next;
-            if (plain) {
-                const int64_t own = a.bin_idx[qid];
-                const int own_cnt = a.bounds[own + 1] - a.bounds[own];
-                R_next = own_cnt > need ? 0 : min(1, R_grid);
-            } else {
-                R_next = R_done;  // certified by construction
-            }
-            while (R_next > R_done) {
-                const bool prune = tau < kInf;
-                scan<NV, DB, CAP>(a, buf, Q, R_done, R_next, prune, m, need, tau, flt, cnt);
-                R_done = R_next;
-                if (R_done >= R_grid) break;
-                if (m >= need) m = compact<NV, CAP>(a, buf, m, need, tau, Q.q, cnt);
-                R_next = tau < kInf ? cover_radius(Q, nb, tau) : R_done + 1;
-            }
-        }
-        bool done = false;
-        if (m > 64 && need <= 63) m = compact<NV, CAP>(a, buf, m, need, tau, Q.q, cnt);
-        if (m <= 64 && need <= 63) done = epilogue_fast<NV, 2, CAP>(a, buf, Q.q, m, need, row_out);
-        if (!done) {
-            ++cnt.exact;
-            epilogue_exact<NV, CAP>(a, buf, Q.q, m, k, row_out);
-        }
-        __syncwarp();
-    }
-    if (a.stats && lane == 0) {
+__device__ __forceinline__ void flush_stats(const KnnArgs& a, int64_t queries, const Counters& cnt) {
+    if (a.stats && lane_id() == 0) {
         atomicAdd(&a.stats[ST_QUERIES], (unsigned long long)queries);
         atomicAdd(&a.stats[ST_REGIONS], (unsigned long long)cnt.regions);
         atomicAdd(&a.stats[ST_CHUNKS], (unsigned long long)cnt.chunks);
@@ -726,6 +742,51 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) k_knn_fwd(KnnArgs a) {
         atomicAdd(&a.stats[ST_EXACT_EPI], (unsigned long long)cnt.exact);
         atomicAdd(&a.stats[ST_ROWS], (unsigned long long)cnt.rows);
     }
+}
+
+// ---------------------------------------------------------------- kernel (one query per warp)
+template <int NV, int DB, int CAP>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, FG_KNN_MINB) k_knn_fwd(KnnArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    WarpBuf<CAP>& buf = reinterpret_cast<WarpBuf<CAP>*>(smem_raw)[threadIdx.x >> 5];
+    const int64_t warp_global = blockIdx.x * (int64_t)kWarpsPerBlock + (threadIdx.x >> 5);
+    const int64_t warps_total = (int64_t)gridDim.x * kWarpsPerBlock;
+    const int need = a.k - 1;
+    const Filter flt = make_filter(a);
+    const float r2_tau = flt.use_r2 ? flt.r2_hi : kInf;
+    const bool exhaustive = a.flags & FG_KNN_EXHAUSTIVE;
+    Counters cnt;
+    int64_t queries = 0;
+    for (int64_t p = warp_global; p < a.n; p += warps_total) {
+        ++queries;
+        const int32_t qid = a.sid[p];
+        const int64_t row_out = (int64_t)qid * a.k;
+        if (begin_row(a, qid, row_out, need, flt)) continue;
+        Query<NV, DB> Q;
+        setup_query(a, p, Q);
+        float tau = r2_tau;
+        int m = 0;
+        if (exhaustive) {
+            scan<NV, DB, CAP>(a, buf, Q, -1, grid_radius(Q, a.nb), false, m, need, tau, flt, cnt);
+        } else {
+            bool done = false;
+            const float tau0 = a.n_c == DB ? density_tau(a, Q, need) : kInf;
+            if (tau0 < tau) {
+                float t0 = tau0;
+                const int R0 = cover_radius(Q, a.nb, tau0);
+                scan<NV, DB, CAP>(a, buf, Q, -1, R0, true, m, need, t0, flt, cnt);
+                if (certified(buf, m, need, tau0)) {
+                    tau = t0;
+                    done = true;
+                } else {
+                    ++cnt.spec_fail;
+                }
+            }
+            if (!done) m = plain_search<NV, DB, CAP>(a, buf, Q, qid, need, flt, tau, cnt);
+        }
+        finish_query<NV, CAP>(a, buf, Q.q, m, need, tau, row_out, cnt);
+    }
+    flush_stats(a, queries, cnt);
 }
 
 template <int NV, int DB, int CAP>

@@ -183,7 +183,8 @@ def _knn_fake(coords, row_splits, bin_idx, sort_order, bin_bounds, dim_mins, wid
 
 
 @torch.library.custom_op(f"{_LIB_NS}::binned_select_knn_grad", mutates_args=())
-def binned_select_knn_grad(grad_d2: Tensor, idx: Tensor, coords: Tensor) -> Tensor:
+def binned_select_knn_grad(grad_d2: Tensor, idx: Tensor, coords: Tensor,
+                           order: Optional[Tensor] = None) -> Tensor:
     _require_cuda(grad_d2, idx, coords)
     L = _lib.load()
     n, n_c = coords.shape
@@ -200,27 +201,33 @@ def binned_select_knn_grad(grad_d2: Tensor, idx: Tensor, coords: Tensor) -> Tens
     grad = torch.empty((n, n_c), dtype=torch.float64 if out_f64 else torch.float32,
                        device=coords.device)
     ws = _ws(_lib.size_out(L.fg_knn_bwd_workspace_size, n, n_c), coords.device)
-    _lib.check(L.fg_knn_bwd(_p(c), n, n_c, _p(ix), k, _p(g), _p(grad), int(out_f64), _p(ws),
-                            ws.numel(), _stream(c)), "binned_select_knn_grad")
+    od = None
+    if order is not None:
+        if order.numel() != n:
+            raise ShapeMismatchError(f"order covers {order.numel()} rows, cloud has {n}")
+        od = order.to(device=coords.device, dtype=torch.int32).contiguous()
+    _lib.check(L.fg_knn_bwd(_p(c), n, n_c, _p(ix), k, _p(g), _p(od), _p(grad), int(out_f64),
+                            _p(ws), ws.numel(), _stream(c)), "binned_select_knn_grad")
     return grad
 
 
 @binned_select_knn_grad.register_fake
-def _knn_grad_fake(grad_d2, idx, coords):
+def _knn_grad_fake(grad_d2, idx, coords, order=None):
     return torch.empty_like(coords)
 
 
 def _knn_setup(ctx, inputs, output):
-    ctx.save_for_backward(inputs[0], output[0])
+    # inputs[3] = sort_order: the backward visits rows in spatial order
+    ctx.save_for_backward(inputs[0], output[0], inputs[3])
     ctx.coords_dtype = inputs[0].dtype
 
 
 def _knn_backward(ctx, grad_idx, grad_d2):
-    coords, idx = ctx.saved_tensors
+    coords, idx, order = ctx.saved_tensors
     if grad_d2 is None:
         g = None
     else:
-        g = binned_select_knn_grad(grad_d2, idx, coords).to(ctx.coords_dtype)
+        g = binned_select_knn_grad(grad_d2, idx, coords, order).to(ctx.coords_dtype)
     return (g,) + (None,) * 14
 
 
