@@ -97,6 +97,24 @@ struct WarpBuf {
     int32_t span_l[32];
 };
 
+template <int NV>
+struct QV {  // query coordinates passed by value (keeps them out of local memory)
+    float v[4 * NV];
+};
+
+template <int NV>
+__device__ __forceinline__ QV<NV> qv_of(const float (&q)[4 * NV]) {
+    QV<NV> r;
+#pragma unroll
+    for (int i = 0; i < 4 * NV; ++i) r.v[i] = q[i];
+    return r;
+}
+
+struct MT {  // (count, tau) result of a compaction
+    int m;
+    float tau;
+};
+
 struct Counters {
     int regions = 0, chunks = 0, appends = 0, compacts = 0, rows = 0, spec_fail = 0, exact = 0;
 };
@@ -175,7 +193,8 @@ __device__ void warp_sort_exact(WarpBuf<CAP>& b, int len) {
 // sentinel), sorted by (d2_f64, original index).
 template <int NV, int CAP>
 __device__ __noinline__ void exact_keys_and_sort(const KnnArgs& a, WarpBuf<CAP>& b, int m,
-                                    const float (&q)[4 * NV]) {
+                                                 const QV<NV> qv) {
+    const float(&q)[4 * NV] = qv.v;
     const int lane = lane_id();
     int len = 32;
     while (len < m) len <<= 1;
@@ -205,10 +224,9 @@ __device__ __noinline__ void exact_keys_and_sort(const KnnArgs& a, WarpBuf<CAP>&
 // ties) keep exactly the `need` best by exact key.  Returns the new count and
 // tightens tau.
 template <int NV, int CAP>
-__device__ __noinline__ int compact(const KnnArgs& a, WarpBuf<CAP>& b, int m, int need, float& tau,
-                       const float (&q)[4 * NV], Counters& cnt) {
+__device__ __noinline__ MT compact_impl(const KnnArgs& a, WarpBuf<CAP>& b, int m, int need,
+                                       float tau, const QV<NV> q) {
     const int lane = lane_id();
-    ++cnt.compacts;
     constexpr int PER = CAP / 32;
     unsigned pref[PER];
     float dv[PER];
@@ -255,7 +273,7 @@ __device__ __noinline__ int compact(const KnnArgs& a, WarpBuf<CAP>& b, int m, in
     }
     tau = nt;
     __syncwarp();
-    if (w <= CAP - 32) return w;
+    if (w <= CAP - 32) return MT{w, tau};
     exact_keys_and_sort<NV, CAP>(a, b, w, q);
     int kept = 0;
     float mx = 0.0f;
@@ -274,7 +292,16 @@ __device__ __noinline__ int compact(const KnnArgs& a, WarpBuf<CAP>& b, int m, in
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(FG_FULL_MASK, mx, o));
     if (kept >= need) tau = fminf(tau, mx * kMargin + kTiny);
     __syncwarp();
-    return kept;
+    return MT{kept, tau};
+}
+
+template <int NV, int CAP>
+__device__ __forceinline__ int compact(const KnnArgs& a, WarpBuf<CAP>& b, int m, int need,
+                                       float& tau, const float (&q)[4 * NV], Counters& cnt) {
+    ++cnt.compacts;
+    const MT r = compact_impl<NV, CAP>(a, b, m, need, tau, qv_of<NV>(q));
+    tau = r.tau;
+    return r.m;
 }
 
 // ---------------------------------------------------------------- geometry
@@ -620,8 +647,8 @@ __device__ bool epilogue_fast(const KnnArgs& a, WarpBuf<CAP>& b, const float (&q
 }
 
 template <int NV, int CAP>
-__device__ __noinline__ void epilogue_exact(const KnnArgs& a, WarpBuf<CAP>& b, const float (&q)[4 * NV], int m,
-                               int k, int64_t row_out) {
+__device__ __noinline__ void epilogue_exact(const KnnArgs& a, WarpBuf<CAP>& b, const QV<NV> q, int m,
+                                            int k, int64_t row_out) {
     const int lane = lane_id();
     exact_keys_and_sort<NV, CAP>(a, b, m, q);
     for (int sl = 1 + lane; sl < k; sl += 32) {
@@ -679,10 +706,19 @@ __device__ __forceinline__ bool begin_row(const KnnArgs& a, int32_t qid, int64_t
 }
 
 // Plain growth from the query's own cell (or its 3^d cube): regions until the
-// cover radius of tau is scanned.  Fills buf, returns the count, sets tau.
+// cover radius of tau is scanned.  Fills buf.  Out of line (rare path), so
+// everything crosses by value: nothing of the hot path becomes address-taken.
+struct PlainOut {
+    int m;
+    float tau;
+    Counters cnt;
+};
+
 template <int NV, int DB, int CAP>
-__device__ __noinline__ int plain_search(const KnnArgs& a, WarpBuf<CAP>& buf, const Query<NV, DB>& Q,
-                            int32_t qid, int need, const Filter& flt, float& tau, Counters& cnt) {
+__device__ __noinline__ PlainOut plain_search(const KnnArgs& a, WarpBuf<CAP>& buf,
+                                              const Query<NV, DB> Q, int32_t qid, int need,
+                                              const Filter flt, float tau) {
+    Counters cnt;
     const int nb = a.nb;
     const int R_grid = grid_radius(Q, nb);
     int m = 0, R_done = -1;
@@ -696,7 +732,17 @@ __device__ __noinline__ int plain_search(const KnnArgs& a, WarpBuf<CAP>& buf, co
         if (m >= need) m = compact<NV, CAP>(a, buf, m, need, tau, Q.q, cnt);
         R_next = tau < kInf ? cover_radius(Q, nb, tau) : R_done + 1;
     }
-    return m;
+    return PlainOut{m, tau, cnt};
+}
+
+__device__ __forceinline__ void add_counters(Counters& c, const Counters& d) {
+    c.regions += d.regions;
+    c.chunks += d.chunks;
+    c.appends += d.appends;
+    c.compacts += d.compacts;
+    c.rows += d.rows;
+    c.spec_fail += d.spec_fail;
+    c.exact += d.exact;
 }
 
 // >= need buffered entries strictly inside tau0 (3e-5 margin): certified.
@@ -717,7 +763,7 @@ __device__ __forceinline__ void finish_query(const KnnArgs& a, WarpBuf<CAP>& buf
     if (m <= 64 && need <= 63) done = epilogue_fast<NV, CAP>(a, buf, q, m, need, row_out);
     if (!done) {
         ++cnt.exact;
-        epilogue_exact<NV, CAP>(a, buf, q, m, a.k, row_out);
+        epilogue_exact<NV, CAP>(a, buf, qv_of<NV>(q), m, a.k, row_out);
     }
     __syncwarp();
 }
@@ -746,7 +792,7 @@ __device__ __forceinline__ void flush_stats(const KnnArgs& a, int64_t queries, c
 
 // ---------------------------------------------------------------- kernel (one query per warp)
 template <int NV, int DB, int CAP>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, FG_KNN_MINB) k_knn_fwd(KnnArgs a) {
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, FG_KNN_MINB) k_knn_fwd(const __grid_constant__ KnnArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     WarpBuf<CAP>& buf = reinterpret_cast<WarpBuf<CAP>*>(smem_raw)[threadIdx.x >> 5];
     const int64_t warp_global = blockIdx.x * (int64_t)kWarpsPerBlock + (threadIdx.x >> 5);
@@ -782,7 +828,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, FG_KNN_MINB) k_knn_fwd(Kn
                     ++cnt.spec_fail;
                 }
             }
-            if (!done) m = plain_search<NV, DB, CAP>(a, buf, Q, qid, need, flt, tau, cnt);
+            if (!done) {
+                const PlainOut po = plain_search<NV, DB, CAP>(a, buf, Q, qid, need, flt, tau);
+                m = po.m;
+                tau = po.tau;
+                add_counters(cnt, po.cnt);
+            }
         }
         finish_query<NV, CAP>(a, buf, Q.q, m, need, tau, row_out, cnt);
     }

@@ -21,6 +21,6 @@ for cfg in sys.argv[1:] or ["north_star", "B", "E", "A"]:
     torch.cuda.synchronize()
     st = ops.knn_stats(reset=True)
     ops.set_debug_flags(0)
-    q = st["queries"]
+    q = max(st["queries"], 1)
     print(cfg, {kk: round(v / q, 3) for kk, v in st.items()}, "per query; cand slots/q =",
           round(32 * st["chunks"] / q, 1))
