@@ -267,23 +267,42 @@ def main():
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    def step(c, u):
+    gravnet = args.config == "E"  # config E: the GravNetOp layer on top of the search
+    if gravnet:
+        n_feat = 64
+        feats = torch.from_numpy(rng.standard_normal((n, n_feat)).astype(np.float32)).to(dev)
+        up_agg = torch.from_numpy(rng.standard_normal((n, 2 * n_feat)).astype(np.float32)).to(dev)
+
+    def step(c, u, f=None, ua=None):
+        """One pass of the path; returns outputs and the phase events."""
+        evs = []
+
+        def mark():
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            evs.append(e)
+
         bi, so, bb, mins, widths, sc = ops.bin_by_coordinates(c, rs, d_bin, n_bins)
-        ev_knn = torch.cuda.Event(enable_timing=True)
-        ev_knn.record(stream)
+        mark()
         idx, d2 = ops.binned_select_knn(c, rs, bi, so, bb, mins, widths, sc, k, d_bin, n_bins,
                                         None, None, False, False)
-        ev_bwd = torch.cuda.Event(enable_timing=True)
-        ev_bwd.record(stream)
+        mark()
+        if gravnet:
+            agg = ops.gravnet_aggregate(f, idx, d2, 10.0, [0, 1], True, so)
+            mark()
+            gf, gd = ops.gravnet_aggregate_grad(ua, f, idx, d2, 10.0, [0, 1], True, so)
+            mark()
+            g = ops.binned_select_knn_grad(gd, idx, c, so)
+            return (idx, d2, g, agg, gf), evs
         g = ops.binned_select_knn_grad(u, idx, c, so)
-        return idx, d2, g, ev_knn, ev_bwd
+        return (idx, d2, g), evs
 
     # warm-up: at least W steps and at least 1.5 s of work, so the SM clocks have
     # left their idle state before anything is timed
     t_warm = time.perf_counter()
     it = 0
     while it < max(args.warmup, 3) or time.perf_counter() - t_warm < 1.5:
-        step(coords, up)
+        step(coords, up, feats if gravnet else None, up_agg if gravnet else None)
         torch.cuda.synchronize()
         it += 1
     torch.cuda.synchronize()
@@ -294,7 +313,10 @@ def main():
                            if os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")[0].isdigit()
                            else local)
     launches0 = _lib.launch_count()
-    t_step = t_bin = t_knn = t_bwd = 0.0
+    names = (["bin_by_coordinates", "knn_fwd", "gravnet_fwd", "gravnet_bwd", "knn_bwd"] if gravnet
+             else ["bin_by_coordinates", "knn_fwd", "knn_bwd"])
+    t_step = 0.0
+    t_phase = [0.0] * len(names)
     with sampler:
         torch.cuda.synchronize()
         if world > 1:
@@ -305,27 +327,28 @@ def main():
             e0 = torch.cuda.Event(enable_timing=True)
             e3 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            idx, d2, g, e1, e2 = step(coords, up)
+            _, evs = step(coords, up, feats if gravnet else None, up_agg if gravnet else None)
             e3.record(stream)
             e3.synchronize()
             t_step += e0.elapsed_time(e3)
-            t_bin += e0.elapsed_time(e1)
-            t_knn += e1.elapsed_time(e2)
-            t_bwd += e2.elapsed_time(e3)
+            marks = [e0] + evs + [e3]
+            for i in range(len(names)):
+                t_phase[i] += marks[i].elapsed_time(marks[i + 1])
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
     launches = _lib.launch_count() - launches0
     clocks = sampler.summary()
 
-    # e2e through the public API with pinned host buffers
+    # e2e through the public API with pinned host buffers: inputs copied in,
+    # every output copied back, inside the timed region
     e2e = None
     if not args.no_e2e:
-        h_coords = torch.from_numpy(coords_np).pin_memory()
-        h_up = torch.from_numpy(up_np).pin_memory()
-        h_idx = torch.empty((n, k), dtype=torch.int32).pin_memory()
-        h_d2 = torch.empty((n, k), dtype=torch.float32).pin_memory()
-        h_g = torch.empty((n, d), dtype=torch.float32).pin_memory()
+        h_in = [torch.from_numpy(coords_np).pin_memory(), torch.from_numpy(up_np).pin_memory()]
+        if gravnet:
+            h_in = [h_in[0], feats.cpu().pin_memory(), up_agg.cpu().pin_memory()]
+        outs, _ = step(coords, up, feats if gravnet else None, up_agg if gravnet else None)
+        h_out = [torch.empty(o.shape, dtype=o.dtype).pin_memory() for o in outs]
         t_e2e = 0.0
         e2e_steps = max(1, min(args.steps, 10))
         for it in range(e2e_steps + 1):
@@ -334,23 +357,23 @@ def main():
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            c = h_coords.to(dev, non_blocking=True)
-            u = h_up.to(dev, non_blocking=True)
-            idx, d2, g, _, _ = step(c, u)
-            h_idx.copy_(idx, non_blocking=True)
-            h_d2.copy_(d2, non_blocking=True)
-            h_g.copy_(g, non_blocking=True)
+            d_in = [h.to(dev, non_blocking=True) for h in h_in]
+            if gravnet:
+                outs, _ = step(d_in[0], None, d_in[1], d_in[2])
+            else:
+                outs, _ = step(d_in[0], d_in[1])
+            for h, o in zip(h_out, outs):
+                h.copy_(o, non_blocking=True)
             e1.record(stream)
             e1.synchronize()
             if it > 0:  # first iteration warms the pinned paths
                 t_e2e += e0.elapsed_time(e1)
         e2e_ms = t_e2e / e2e_steps
-        h2d = h_coords.numel() * 4 + h_up.numel() * 4
-        d2h = h_idx.numel() * 4 + h_d2.numel() * 4 + h_g.numel() * 4
+        h2d = sum(h.numel() * h.element_size() for h in h_in)
+        d2h = sum(h.numel() * h.element_size() for h in h_out)
         e2e = [e2e_ms, h2d, d2h]
 
-    per_rank = [t_step / args.steps, t_bin / args.steps, t_knn / args.steps, t_bwd / args.steps,
-                n, e2e[0] if e2e else 0.0]
+    per_rank = [t_step / args.steps, n, e2e[0] if e2e else 0.0] + [t / args.steps for t in t_phase]
     allr = sharding.gather_floats(per_rank)
     if rank != 0:
         if world > 1:
@@ -358,14 +381,18 @@ def main():
             dist.destroy_process_group()
         return 0
     ms = float(allr[:, 0].max())
-    total_q = float(allr[:, 4].sum())
+    total_q = float(allr[:, 1].sum())
+    phase = {nm: float(allr[0, 3 + i]) for i, nm in enumerate(names)}
     value = total_q / (ms * 1e-3)
     peak, peak_src = load_peak()
     c_total = C_TOTAL[args.config]
     if args.config == "D":
         c_total = C_TOTAL["D"] * (n / 6_400_000)
     b_fwd, b_bwd = algorithmic_bytes(n, d, k, c_total)
-    t_knn_ms = float(allr[0, 2])
+    if gravnet:  # B_agg = (8Nk + 4NkF + 8NF) + (8NF + 8Nk + 8NkF + 4Nk)
+        F = 64
+        b_bwd += (8 * n * k + 4 * n * k * F + 8 * n * F) + (8 * n * F + 8 * n * k + 8 * n * k * F + 4 * n * k)
+    t_knn_ms = phase["knn_fwd"]
     achieved = b_fwd / (t_knn_ms * 1e-3) / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
@@ -376,8 +403,7 @@ def main():
                    "d_bin": d_bin, "events": world if scaling == "weak" else 64,
                    "l2": "no flush" if args.no_flush else "flushed (256 MiB write) before every step",
                    "precision": "fp32 distance filter, float64 exact epilogue / gradient sums"},
-        "breakdown_ms": {"bin_by_coordinates": float(allr[0, 1]), "knn_fwd": t_knn_ms,
-                         "knn_bwd": float(allr[0, 3])},
+        "breakdown_ms": phase,
         "roofline": {"bound": "hbm", "kernel": "k_knn_fwd", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": load_traffic(args.config),
                      "peak_source": peak_src,
@@ -388,7 +414,7 @@ def main():
         "clocks": clocks,
     }
     if e2e:
-        e2e_ms = float(allr[:, 5].max())
+        e2e_ms = float(allr[:, 2].max())
         line["e2e"] = {"value": total_q / (e2e_ms * 1e-3), "unit": "queries/s",
                        "h2d_bytes_per_step": int(e2e[1]), "d2h_bytes_per_step": int(e2e[2]),
                        "ms_per_step": e2e_ms}

@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define FG_ABI_VERSION 1
+#define FG_ABI_VERSION 2
 
 enum fg_status {
     FG_OK = 0,
@@ -135,21 +135,26 @@ int fg_knn_bwd(const float *coords, int64_t n, int32_t n_coords, const int32_t *
 /* gravnet_aggregate.  Replaces G/gravnet.py:64-97: per vertex, weights
  * w = exp(-scale*d2) over valid slots (idx >= 0, slot 0 only with
  * include_self), reducers applied in order (FG_REDUCE_*), one F-wide block
- * each: out[n, F*n_reducers] float32.  Arithmetic in float64. */
+ * each: out[n, F*n_reducers] float32.  Arithmetic in float64.  `order`
+ * (optional, may be NULL) is a permutation of the rows to visit them in --
+ * the bin index's sort_order makes neighbouring warps share feature rows. */
 int fg_gravnet_fwd(const float *feats, int64_t n, int32_t n_feats, const int32_t *idx,
                    const float *d2, int32_t k, double weight_scale, const int32_t *reducers,
-                   int32_t n_reducers, int32_t include_self, float *out, void *stream);
+                   int32_t n_reducers, int32_t include_self, const int32_t *order, float *out,
+                   void *stream);
 
-int fg_gravnet_bwd_workspace_size(int64_t n, int32_t n_feats, size_t *bytes);
+int fg_gravnet_bwd_workspace_size(int64_t n, int32_t n_feats, int32_t k, size_t *bytes);
 
 /* gravnet_aggregate_backward.  Replaces G/gravnet.py:100-150 ->
  * (grad_feats[n,F] float32, grad_d2[n,k] float32); max blocks route to the
- * lowest arg-max slot. */
+ * lowest arg-max slot.  No floating-point atomics: grad_d2 comes from a row
+ * pass, grad_feats from a pass over each vertex's reverse-neighbour list
+ * (built in the workspace), both float64 inside.  k <= 65535, n*k < 2^31. */
 int fg_gravnet_bwd(const float *feats, int64_t n, int32_t n_feats, const int32_t *idx,
                    const float *d2, int32_t k, double weight_scale, const int32_t *reducers,
-                   int32_t n_reducers, int32_t include_self, const float *upstream,
-                   float *grad_feats, float *grad_d2, void *workspace, size_t workspace_bytes,
-                   void *stream);
+                   int32_t n_reducers, int32_t include_self, const int32_t *order,
+                   const float *upstream, float *grad_feats, float *grad_d2, void *workspace,
+                   size_t workspace_bytes, void *stream);
 
 /* ---------------------------------------------------------------- misc */
 

@@ -50,9 +50,10 @@ _SIGS = {
     "fg_knn_bwd_workspace_size": ([_I64, _I32, _SZ], ctypes.c_int),
     "fg_knn_bwd": ([_P, _I64, _I32, _P, _I32, _P, _P, _P, _I32, _P, ctypes.c_size_t, _P],
                    ctypes.c_int),
-    "fg_gravnet_fwd": ([_P, _I64, _I32, _P, _P, _I32, _D, _P, _I32, _I32, _P, _P], ctypes.c_int),
-    "fg_gravnet_bwd_workspace_size": ([_I64, _I32, _SZ], ctypes.c_int),
-    "fg_gravnet_bwd": ([_P, _I64, _I32, _P, _P, _I32, _D, _P, _I32, _I32, _P, _P, _P, _P,
+    "fg_gravnet_fwd": ([_P, _I64, _I32, _P, _P, _I32, _D, _P, _I32, _I32, _P, _P, _P],
+                       ctypes.c_int),
+    "fg_gravnet_bwd_workspace_size": ([_I64, _I32, _I32, _SZ], ctypes.c_int),
+    "fg_gravnet_bwd": ([_P, _I64, _I32, _P, _P, _I32, _D, _P, _I32, _I32, _P, _P, _P, _P, _P,
                         ctypes.c_size_t, _P], ctypes.c_int),
     "fg_error_string": ([ctypes.c_int], ctypes.c_char_p),
     "fg_abi_version": ([], ctypes.c_int),

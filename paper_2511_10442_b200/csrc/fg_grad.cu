@@ -1,14 +1,11 @@
-// fg_grad.cu -- binned_select_knn backward (replaces G/knn.py:135-168) and the
-// GravNet distance-weighted aggregation forward/backward (replaces
-// G/gravnet.py:64-150) for sm_100a.
+// fg_grad.cu -- binned_select_knn backward (replaces G/knn.py:135-168) for
+// sm_100a.
 //
 // Precision: every knn_backward term 2g(x_v - x_u) is formed exactly in float64
 // (fp32 g and x), the query-side sum of a row is a warp reduction in float64,
 // and both sides reach the per-vertex accumulator through compensated fp32x4
 // atomics (hi + exact-TwoSum error, see two_sum_add): ~2^-48 relative to the
-// term magnitudes, i.e. float64-class, then rounded once to the output type.  GravNet weights exp(-scale d2), the
-// weighted terms, sums and maxima are float64 and stored
-// as float32.
+// term magnitudes, i.e. float64-class, then rounded once to the output type.
 #include "fg_common.cuh"
 
 namespace fg {
@@ -114,143 +111,6 @@ __global__ void k_bwd_finish(const float4* __restrict__ hi, const float4* __rest
     }
 }
 
-__global__ void k_round_out(const double* __restrict__ acc, int64_t m, void* __restrict__ out, int is_f64) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        if (is_f64)
-            reinterpret_cast<double*>(out)[i] = acc[i];
-        else
-            reinterpret_cast<float*>(out)[i] = (float)acc[i];
-    }
-}
-
-// ---------------------------------------------------------------- GravNet
-// Warp per vertex; lanes over features (FPL features per lane per pass).
-__global__ void __launch_bounds__(kRowWarps * 32) k_gravnet_fwd(const float* __restrict__ feats, int64_t n,
-                                                              int F, const int32_t* __restrict__ idx,
-                                                              const float* __restrict__ d2, int k,
-                                                              double scale, int4 red, int n_red,
-                                                              int include_self, float* __restrict__ out) {
-    const int lane = lane_id();
-    const int64_t v = blockIdx.x * (int64_t)kRowWarps + (threadIdx.x >> 5);
-    if (v >= n) return;
-    const int W = F * n_red;
-    int cnt = 0;
-    for (int base = 0; base < k; base += 32) {
-        const int s = base + lane;
-        const bool ok = s < k && idx[v * k + s] >= 0 && (include_self || s > 0);
-        cnt += __popc(__ballot_sync(FG_FULL_MASK, ok));
-    }
-    const int reds[4] = {red.x, red.y, red.z, red.w};
-    for (int f0 = 0; f0 < F; f0 += 32) {
-        const int f = f0 + lane;
-        double sum = 0.0, mx = -INFINITY;
-        for (int base = 0; base < k; base += 32) {
-            const int s = base + lane;
-            int32_t u = s < k ? idx[v * k + s] : -1;
-            const bool ok = u >= 0 && (include_self || s > 0);
-            const double w = ok ? exp(-scale * (double)d2[v * k + s]) : 0.0;
-            const unsigned okm = __ballot_sync(FG_FULL_MASK, ok);
-            const int lim = min(32, k - base);
-            for (int j = 0; j < lim; ++j) {
-                if (!((okm >> j) & 1u)) continue;
-                const int32_t uj = __shfl_sync(FG_FULL_MASK, u, j);
-                const double wj = __shfl_sync(FG_FULL_MASK, w, j);
-                if (f < F) {
-                    const double term = wj * (double)feats[(int64_t)uj * F + f];
-                    sum += term;
-                    if (term > mx) mx = term;
-                }
-            }
-        }
-        if (f < F) {
-            for (int b = 0; b < n_red; ++b) {
-                double val = 0.0;
-                if (cnt > 0) val = reds[b] == FG_REDUCE_MEAN ? sum / (double)cnt : mx;
-                out[v * W + (int64_t)b * F + f] = (float)val;
-            }
-        }
-    }
-}
-
-// grad_feats via float64 atomics into gacc[n*F]; grad_d2 per row in smem.
-__global__ void __launch_bounds__(kRowWarps * 32) k_gravnet_bwd(const float* __restrict__ feats, int64_t n,
-                                                              int F, const int32_t* __restrict__ idx,
-                                                              const float* __restrict__ d2, int k,
-                                                              double scale, int4 red, int n_red,
-                                                              int include_self,
-                                                              const float* __restrict__ up,
-                                                              double* __restrict__ gacc,
-                                                              float* __restrict__ grad_d2) {
-    extern __shared__ double s_gd[];
-    const int lane = lane_id();
-    const int wib = threadIdx.x >> 5;
-    double* gd = s_gd + (size_t)wib * k;
-    const int64_t v = blockIdx.x * (int64_t)kRowWarps + wib;
-    if (v >= n) return;
-    const int W = F * n_red;
-    for (int s = lane; s < k; s += 32) gd[s] = 0.0;
-    int cnt = 0;
-    for (int base = 0; base < k; base += 32) {
-        const int s = base + lane;
-        const bool ok = s < k && idx[v * k + s] >= 0 && (include_self || s > 0);
-        cnt += __popc(__ballot_sync(FG_FULL_MASK, ok));
-    }
-    __syncwarp();
-    const int reds[4] = {red.x, red.y, red.z, red.w};
-    if (cnt > 0) {
-        for (int b = 0; b < n_red; ++b) {
-            const bool is_mean = reds[b] == FG_REDUCE_MEAN;
-            for (int f0 = 0; f0 < F; f0 += 32) {
-                const int f = f0 + lane;
-                const double g = f < F ? (double)up[v * W + (int64_t)b * F + f] : 0.0;
-                const double coeff = g / (double)cnt;
-                double best = -INFINITY;
-                int best_s = -1;
-                int32_t best_u = 0;
-                double best_w = 0.0;
-                for (int base = 0; base < k; base += 32) {
-                    const int s = base + lane;
-                    const int32_t u = s < k ? idx[v * k + s] : -1;
-                    const bool ok = u >= 0 && (include_self || s > 0);
-                    const double w = ok ? exp(-scale * (double)d2[v * k + s]) : 0.0;
-                    const unsigned okm = __ballot_sync(FG_FULL_MASK, ok);
-                    const int lim = min(32, k - base);
-                    for (int j = 0; j < lim; ++j) {
-                        if (!((okm >> j) & 1u)) continue;
-                        const int32_t uj = __shfl_sync(FG_FULL_MASK, u, j);
-                        const double wj = __shfl_sync(FG_FULL_MASK, w, j);
-                        const double fv = f < F ? (double)feats[(int64_t)uj * F + f] : 0.0;
-                        if (is_mean) {
-                            if (f < F) atomicAdd(&gacc[(int64_t)uj * F + f], wj * coeff);
-                            double dot = fv * coeff;
-#pragma unroll
-                            for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(FG_FULL_MASK, dot, o);
-                            if (lane == 0) gd[base + j] += -scale * wj * dot;
-                        } else {
-                            const double term = wj * fv;
-                            if (f < F && term > best) {
-                                best = term;
-                                best_s = base + j;
-                                best_u = uj;
-                                best_w = wj;
-                            }
-                        }
-                    }
-                    __syncwarp();
-                }
-                if (!is_mean && f < F && best_s >= 0) {
-                    atomicAdd(&gacc[(int64_t)best_u * F + f], g * best_w);
-                    atomicAdd(&gd[best_s], ((-scale * g) * best_w) * (double)feats[(int64_t)best_u * F + f]);
-                }
-                __syncwarp();
-            }
-        }
-    }
-    __syncwarp();
-    for (int s = lane; s < k; s += 32) grad_d2[v * k + s] = (float)gd[s];
-}
-
 }  // namespace grad
 }  // namespace fg
 
@@ -292,70 +152,5 @@ extern "C" int fg_knn_bwd(const float* coords, int64_t n, int32_t n_coords, cons
     const int64_t m = n * n_coords;
     k_bwd_finish<<<(unsigned)std::min<int64_t>(ceil_div(m, 256), 148 * 16), 256, 0, st>>>(
         hi, lo, n, n_coords, nv, grad_coords, grad_is_f64);
-    return launched(st);
-}
-
-static int check_reducers(const int32_t* reducers, int32_t n_red, int4* red) {
-    if (!reducers) return FG_ERR_NULL;
-    if (n_red < 1 || n_red > 4) return FG_ERR_BAD_SHAPE;
-    int r[4] = {0, 0, 0, 0};
-    for (int i = 0; i < n_red; ++i) {
-        if (reducers[i] != FG_REDUCE_MEAN && reducers[i] != FG_REDUCE_MAX) return FG_ERR_BAD_SHAPE;
-        r[i] = reducers[i];
-    }
-    *red = make_int4(r[0], r[1], r[2], r[3]);
-    return 0;
-}
-
-extern "C" int fg_gravnet_fwd(const float* feats, int64_t n, int32_t n_feats, const int32_t* idx,
-                              const float* d2, int32_t k, double weight_scale,
-                              const int32_t* reducers, int32_t n_reducers, int32_t include_self,
-                              float* out, void* stream) {
-    int4 red;
-    FG_TRY(check_reducers(reducers, n_reducers, &red));
-    if (k < 1) return FG_ERR_BAD_K;
-    if (n < 0 || n_feats < 1) return FG_ERR_BAD_SHAPE;
-    if (!(weight_scale > 0.0)) return FG_ERR_BAD_SHAPE;
-    if (n == 0) return 0;
-    if (!feats || !idx || !d2 || !out) return FG_ERR_NULL;
-    cudaStream_t st = (cudaStream_t)stream;
-    k_gravnet_fwd<<<(unsigned)ceil_div(n, kRowWarps), kRowWarps * 32, 0, st>>>(
-        feats, n, n_feats, idx, d2, k, weight_scale, red, n_reducers, include_self, out);
-    return launched(st);
-}
-
-extern "C" int fg_gravnet_bwd_workspace_size(int64_t n, int32_t n_feats, size_t* bytes) {
-    if (!bytes) return FG_ERR_NULL;
-    if (n < 0 || n_feats < 1) return FG_ERR_BAD_SHAPE;
-    *bytes = align_up(sizeof(double) * (size_t)n * n_feats, 256);
-    return 0;
-}
-
-extern "C" int fg_gravnet_bwd(const float* feats, int64_t n, int32_t n_feats, const int32_t* idx,
-                              const float* d2, int32_t k, double weight_scale,
-                              const int32_t* reducers, int32_t n_reducers, int32_t include_self,
-                              const float* upstream, float* grad_feats, float* grad_d2,
-                              void* workspace, size_t workspace_bytes, void* stream) {
-    int4 red;
-    FG_TRY(check_reducers(reducers, n_reducers, &red));
-    if (k < 1 || k > 4096) return FG_ERR_BAD_K;
-    if (n < 0 || n_feats < 1) return FG_ERR_BAD_SHAPE;
-    if (!(weight_scale > 0.0)) return FG_ERR_BAD_SHAPE;
-    if (n == 0) return 0;
-    if (!feats || !idx || !d2 || !upstream || !grad_feats || !grad_d2 || !workspace) return FG_ERR_NULL;
-    const size_t need = align_up(sizeof(double) * (size_t)n * n_feats, 256);
-    if (workspace_bytes < need) return FG_ERR_WORKSPACE;
-    cudaStream_t st = (cudaStream_t)stream;
-    double* gacc = (double*)workspace;
-    FG_CUDA(cudaMemsetAsync(gacc, 0, sizeof(double) * (size_t)n * n_feats, st));
-    const size_t smem = sizeof(double) * (size_t)k * kRowWarps;
-    if (smem > 48 * 1024)
-        FG_CUDA(cudaFuncSetAttribute(k_gravnet_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_gravnet_bwd<<<(unsigned)ceil_div(n, kRowWarps), kRowWarps * 32, smem, st>>>(
-        feats, n, n_feats, idx, d2, k, weight_scale, red, n_reducers, include_self, upstream, gacc,
-        grad_d2);
-    FG_TRY(launched(st));
-    const int64_t m = n * n_feats;
-    k_round_out<<<(unsigned)std::min<int64_t>(ceil_div(m, 256), 148 * 8), 256, 0, st>>>(gacc, m, grad_feats, 0);
     return launched(st);
 }

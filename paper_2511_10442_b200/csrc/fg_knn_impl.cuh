@@ -48,6 +48,15 @@
 #ifndef FG_SPAN_WALK
 #define FG_SPAN_WALK 0
 #endif
+#ifndef FG_EPI_BITONIC
+#define FG_EPI_BITONIC 0
+#endif
+#ifndef FG_EPI_CUT
+#define FG_EPI_CUT 64
+#endif
+#ifndef FG_ALPHA
+#define FG_ALPHA 1.07f
+#endif
 #ifndef FG_KNN_MINB
 #define FG_KNN_MINB 8
 #endif
@@ -61,7 +70,7 @@ constexpr int kWarpsPerBlock = 4;
 constexpr float kMargin = 1.0f + 1e-5f;
 constexpr float kTiny = 1e-35f;
 constexpr float kCellSlack = 1e-4f;  // cell units
-constexpr float kAlpha = 1.07f;      // speculative radius inflation
+constexpr float kAlpha = FG_ALPHA;   // speculative radius inflation
 constexpr float kInf = __builtin_huge_valf();
 
 enum { ST_QUERIES, ST_REGIONS, ST_CHUNKS, ST_APPENDS, ST_COMPACT, ST_SPEC_FAIL, ST_EXACT_EPI,
@@ -646,6 +655,94 @@ __device__ bool epilogue_fast(const KnnArgs& a, WarpBuf<CAP>& b, const float (&q
     return true;
 }
 
+// Alternative fast path: register bitonic sort of (float32(d2_f64), position),
+// E keys per lane (FG_EPI_BITONIC).
+template <int NV, int E, int CAP>
+__device__ bool epilogue_bitonic(const KnnArgs& a, WarpBuf<CAP>& b, const float (&q)[4 * NV], int m,
+                              int need, int64_t row_out) {
+    constexpr int N = 32 * E;
+    const int lane = lane_id();
+    const bool use_r2 = a.flags & FG_KNN_USE_MAX_R2;
+    unsigned kx[E];  // float32(d2_f64) bits (monotone for d2 >= 0); invalid = ~0
+    int32_t px[E];   // sorted position
+#pragma unroll
+    for (int t = 0; t < E; ++t) {
+        const int e = E * lane + t;
+        kx[t] = ~0u;
+        px[t] = -1;
+        if (e < m) {
+            const int32_t cpos = b.p[e];
+            const double d = exact_pos_d2<NV>(a, q, cpos);
+            if (!use_r2 || d <= a.max_r2) {
+                kx[t] = __float_as_uint(__double2float_rn(d));
+                px[t] = cpos;
+            }
+        }
+    }
+#pragma unroll
+    for (int k2 = 2; k2 <= N; k2 <<= 1) {
+#pragma unroll
+        for (int j2 = k2 >> 1; j2 > 0; j2 >>= 1) {
+            if (j2 < E) {
+#pragma unroll
+                for (int t = 0; t < E; ++t) {
+                    if ((t & j2) == 0) {
+                        const int u = t | j2;
+                        const bool asc = ((E * lane + t) & k2) == 0;
+                        const bool sw = asc ? (kx[t] > kx[u]) : (kx[t] < kx[u]);
+                        const unsigned k0 = sw ? kx[u] : kx[t], k1 = sw ? kx[t] : kx[u];
+                        const int32_t p0 = sw ? px[u] : px[t], p1 = sw ? px[t] : px[u];
+                        kx[t] = k0; kx[u] = k1; px[t] = p0; px[u] = p1;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int t = 0; t < E; ++t) {
+                    const int i = E * lane + t;
+                    const unsigned ok = __shfl_xor_sync(FG_FULL_MASK, kx[t], j2 / E);
+                    const int32_t op = __shfl_xor_sync(FG_FULL_MASK, px[t], j2 / E);
+                    const bool keep_min = ((i & j2) == 0) == ((i & k2) == 0);
+                    const bool take = keep_min ? (ok < kx[t]) : (ok > kx[t]);
+                    kx[t] = take ? ok : kx[t];
+                    px[t] = take ? op : px[t];
+                }
+            }
+        }
+    }
+    // entries that decide the row: pairs (i, i+1) with i + 1 <= need
+    bool amb = false;
+#pragma unroll
+    for (int t = 0; t + 1 < E; ++t) {
+        const int i = E * lane + t;
+        amb |= i + 1 <= need && kx[t + 1] != ~0u && kx[t] == kx[t + 1];
+    }
+    {
+        const unsigned nxt = __shfl_down_sync(FG_FULL_MASK, kx[0], 1);
+        const int i = E * lane + E - 1;
+        amb |= lane < 31 && i + 1 <= need && nxt != ~0u && kx[E - 1] == nxt;
+    }
+    if (__any_sync(FG_FULL_MASK, amb)) return false;
+    const bool f64 = a.flags & FG_KNN_D2_F64;
+#pragma unroll
+    for (int t = 0; t < E; ++t) {
+        const int i = E * lane + t;
+        if (i < need) {
+            const int64_t off = row_out + 1 + i;
+            if (kx[t] != ~0u) {
+                a.out_idx[off] = a.sid[px[t]];
+                if (f64)
+                    reinterpret_cast<double*>(a.out_d2)[off] = exact_pos_d2<NV>(a, q, px[t]);
+                else
+                    reinterpret_cast<float*>(a.out_d2)[off] = __uint_as_float(kx[t]);
+            } else {
+                a.out_idx[off] = -1;
+                store_d2(a, off, 0.0);
+            }
+        }
+    }
+    return true;
+}
+
 template <int NV, int CAP>
 __device__ __noinline__ void epilogue_exact(const KnnArgs& a, WarpBuf<CAP>& b, const QV<NV> q, int m,
                                             int k, int64_t row_out) {
@@ -759,8 +856,12 @@ __device__ __forceinline__ void finish_query(const KnnArgs& a, WarpBuf<CAP>& buf
                                              const float (&q)[4 * NV], int m, int need, float tau,
                                              int64_t row_out, Counters& cnt) {
     bool done = false;
-    if (m > 64 && need <= 63) m = compact<NV, CAP>(a, buf, m, need, tau, q, cnt);
+    if (m > FG_EPI_CUT && need <= 63) m = compact<NV, CAP>(a, buf, m, need, tau, q, cnt);
+#if FG_EPI_BITONIC
+    if (m <= 64 && need <= 63) done = epilogue_bitonic<NV, 2, CAP>(a, buf, q, m, need, row_out);
+#else
     if (m <= 64 && need <= 63) done = epilogue_fast<NV, CAP>(a, buf, q, m, need, row_out);
+#endif
     if (!done) {
         ++cnt.exact;
         epilogue_exact<NV, CAP>(a, buf, qv_of<NV>(q), m, a.k, row_out);

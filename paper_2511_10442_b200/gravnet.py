@@ -70,16 +70,17 @@ def neighbor_weights(neighbors: NeighborMatrix, spec: AggregationSpec):
 
 
 def gravnet_aggregate(features, neighbors: NeighborMatrix,
-                      spec: AggregationSpec = AggregationSpec()) -> torch.Tensor:
+                      spec: AggregationSpec = AggregationSpec(), order=None) -> torch.Tensor:
     """(n_vertices, n_features * n_reducers); differentiable w.r.t. features
-    and neighbors.dist2."""
+    and neighbors.dist2.  ``order`` (optional, e.g. the bin index's
+    sort_order) only changes the order rows are visited in, not the result."""
     f = _check_features(features, neighbors)
     return ops.gravnet_aggregate(f, neighbors.indices, neighbors.dist2, float(spec.weight_scale),
-                                 spec.codes, bool(spec.include_self))
+                                 spec.codes, bool(spec.include_self), order)
 
 
 def gravnet_aggregate_backward(features, neighbors: NeighborMatrix, spec: AggregationSpec,
-                               upstream) -> tuple[torch.Tensor, torch.Tensor]:
+                               upstream, order=None) -> tuple[torch.Tensor, torch.Tensor]:
     """G/gravnet.py:100-150 -> (grad_features, grad_dist2)."""
     f = _check_features(features, neighbors)
     want = (f.shape[0], f.shape[1] * len(spec.reducers))
@@ -87,7 +88,7 @@ def gravnet_aggregate_backward(features, neighbors: NeighborMatrix, spec: Aggreg
         raise ShapeMismatchError(f"upstream shape {tuple(upstream.shape)} != {want}")
     return ops.gravnet_aggregate_grad(upstream, f, neighbors.indices, neighbors.dist2,
                                       float(spec.weight_scale), spec.codes,
-                                      bool(spec.include_self))
+                                      bool(spec.include_self), order)
 
 
 class GravNetOp(nn.Module):
@@ -116,8 +117,8 @@ class GravNetOp(nn.Module):
             self.out = nn.Linear(in_features + n_prop * len(reducers), out_features)
 
     def aggregate(self, coords: torch.Tensor, feats: torch.Tensor, row_splits):
-        idx, d2 = select_knn(coords, row_splits, self.k)
-        agg = gravnet_aggregate(feats, NeighborMatrix(idx, d2), self.spec)
+        idx, d2, order = select_knn(coords, row_splits, self.k, return_order=True)
+        agg = gravnet_aggregate(feats, NeighborMatrix(idx, d2), self.spec, order)
         return agg, idx, d2
 
     def forward(self, x: torch.Tensor, row_splits, feats: torch.Tensor | None = None):

@@ -120,12 +120,16 @@ def knn_with_grad(cloud: PointCloud, index: BinIndex, opts: KnnOptions):
 
 def select_knn(coords: torch.Tensor, row_splits, K: int, *, direction=None,
                max_radius2: float | None = None, n_bins: int | None = None,
-               d_bin: int | None = None):
+               d_bin: int | None = None, return_order: bool = False):
     """One-call FastGraph-style API: bin + search, differentiable w.r.t.
-    ``coords``.  Returns (idx int32 [N, K], d2 float32 [N, K])."""
+    ``coords``.  Returns (idx int32 [N, K], d2 float32 [N, K]), plus the bin
+    index's sort_order (a spatially coherent row order for follow-up kernels)
+    when ``return_order``."""
     cloud = PointCloud(coords, row_splits, check_finite=False)
     cfg = BinningConfig(k_target=int(K), d_bin=d_bin, n_bins=n_bins)
     index = build_bin_index(cloud, cfg)
     mask = None if direction is None else DirectionMask(direction)
     nm = binned_select_knn(cloud, index, KnnOptions(k=int(K), mask=mask, max_radius2=max_radius2))
+    if return_order:
+        return nm.indices, nm.dist2, index.sort_order
     return nm.indices, nm.dist2

@@ -55,6 +55,15 @@ def knn_stats(reset: bool = True) -> dict:
     return dict(zip(names, [int(x) for x in buf]))
 
 
+def _order(order: Optional[Tensor], n: int, device) -> Optional[Tensor]:
+    """Validated int32 device copy of an optional row visit order."""
+    if order is None:
+        return None
+    if order.numel() != n:
+        raise ShapeMismatchError(f"order covers {order.numel()} rows, there are {n}")
+    return order.to(device=device, dtype=torch.int32).contiguous()
+
+
 def _p(t: Optional[Tensor]):
     if t is None or t.numel() == 0:
         return None
@@ -201,11 +210,7 @@ def binned_select_knn_grad(grad_d2: Tensor, idx: Tensor, coords: Tensor,
     grad = torch.empty((n, n_c), dtype=torch.float64 if out_f64 else torch.float32,
                        device=coords.device)
     ws = _ws(_lib.size_out(L.fg_knn_bwd_workspace_size, n, n_c), coords.device)
-    od = None
-    if order is not None:
-        if order.numel() != n:
-            raise ShapeMismatchError(f"order covers {order.numel()} rows, cloud has {n}")
-        od = order.to(device=coords.device, dtype=torch.int32).contiguous()
+    od = _order(order, n, coords.device)
     _lib.check(L.fg_knn_bwd(_p(c), n, n_c, _p(ix), k, _p(g), _p(od), _p(grad), int(out_f64),
                             _p(ws), ws.numel(), _stream(c)), "binned_select_knn_grad")
     return grad
@@ -241,7 +246,9 @@ def _check_red(reducers: Sequence[int]) -> Tensor:
 
 @torch.library.custom_op(f"{_LIB_NS}::gravnet_aggregate", mutates_args=())
 def gravnet_aggregate(feats: Tensor, idx: Tensor, d2: Tensor, weight_scale: float,
-                      reducers: list[int], include_self: bool) -> Tensor:
+                      reducers: list[int], include_self: bool,
+                      order: Optional[Tensor] = None) -> Tensor:
+    """``order`` (optional): row visit order, e.g. the bin index's sort_order."""
     _require_cuda(feats, idx, d2)
     n, F = feats.shape
     k = idx.shape[1]
@@ -249,23 +256,25 @@ def gravnet_aggregate(feats: Tensor, idx: Tensor, d2: Tensor, weight_scale: floa
     ix = idx.to(torch.int32).contiguous()
     dd = d2.to(torch.float32).contiguous()
     red = _check_red(reducers)
+    od = _order(order, n, feats.device)
     out = torch.empty((n, F * red.numel()), dtype=torch.float32, device=feats.device)
     _lib.check(_lib.load().fg_gravnet_fwd(_p(f), n, F, _p(ix), _p(dd), k, float(weight_scale),
                                           ctypes.c_void_p(red.data_ptr()), red.numel(),
-                                          int(include_self), _p(out), _stream(f)),
+                                          int(include_self), _p(od), _p(out),
+                                          _stream(f)),
                "gravnet_aggregate")
     return out
 
 
 @gravnet_aggregate.register_fake
-def _gn_fake(feats, idx, d2, weight_scale, reducers, include_self):
+def _gn_fake(feats, idx, d2, weight_scale, reducers, include_self, order=None):
     return feats.new_empty((feats.shape[0], feats.shape[1] * len(reducers)), dtype=torch.float32)
 
 
 @torch.library.custom_op(f"{_LIB_NS}::gravnet_aggregate_grad", mutates_args=())
 def gravnet_aggregate_grad(grad_out: Tensor, feats: Tensor, idx: Tensor, d2: Tensor,
-                           weight_scale: float, reducers: list[int],
-                           include_self: bool) -> tuple[Tensor, Tensor]:
+                           weight_scale: float, reducers: list[int], include_self: bool,
+                           order: Optional[Tensor] = None) -> tuple[Tensor, Tensor]:
     _require_cuda(grad_out, feats, idx, d2)
     L = _lib.load()
     n, F = feats.shape
@@ -277,34 +286,36 @@ def gravnet_aggregate_grad(grad_out: Tensor, feats: Tensor, idx: Tensor, d2: Ten
     ix = idx.to(torch.int32).contiguous()
     dd = d2.to(torch.float32).contiguous()
     up = grad_out.to(torch.float32).contiguous()
+    od = _order(order, n, feats.device)
     gf = torch.empty((n, F), dtype=torch.float32, device=feats.device)
     gd = torch.empty((n, k), dtype=torch.float32, device=feats.device)
-    ws = _ws(_lib.size_out(L.fg_gravnet_bwd_workspace_size, n, F), feats.device)
+    ws = _ws(_lib.size_out(L.fg_gravnet_bwd_workspace_size, n, F, k), feats.device)
     _lib.check(L.fg_gravnet_bwd(_p(f), n, F, _p(ix), _p(dd), k, float(weight_scale),
                                 ctypes.c_void_p(red.data_ptr()), red.numel(), int(include_self),
-                                _p(up), _p(gf), _p(gd), _p(ws), ws.numel(), _stream(f)),
+                                _p(od), _p(up), _p(gf), _p(gd), _p(ws), ws.numel(),
+                                _stream(f)),
                "gravnet_aggregate_grad")
     return gf, gd
 
 
 @gravnet_aggregate_grad.register_fake
-def _gn_grad_fake(grad_out, feats, idx, d2, weight_scale, reducers, include_self):
+def _gn_grad_fake(grad_out, feats, idx, d2, weight_scale, reducers, include_self, order=None):
     return (torch.empty_like(feats, dtype=torch.float32),
             torch.empty_like(d2, dtype=torch.float32))
 
 
 def _gn_setup(ctx, inputs, output):
-    feats, idx, d2, scale, reducers, include_self = inputs
-    ctx.save_for_backward(feats, idx, d2)
+    feats, idx, d2, scale, reducers, include_self, order = inputs
+    ctx.save_for_backward(feats, idx, d2, order)
     ctx.args = (scale, list(reducers), include_self)
     ctx.dtypes = (feats.dtype, d2.dtype)
 
 
 def _gn_backward(ctx, grad_out):
-    feats, idx, d2 = ctx.saved_tensors
+    feats, idx, d2, order = ctx.saved_tensors
     scale, reducers, include_self = ctx.args
-    gf, gd = gravnet_aggregate_grad(grad_out, feats, idx, d2, scale, reducers, include_self)
-    return gf.to(ctx.dtypes[0]), None, gd.to(ctx.dtypes[1]), None, None, None
+    gf, gd = gravnet_aggregate_grad(grad_out, feats, idx, d2, scale, reducers, include_self, order)
+    return gf.to(ctx.dtypes[0]), None, gd.to(ctx.dtypes[1]), None, None, None, None
 
 
 gravnet_aggregate.register_autograd(_gn_backward, setup_context=_gn_setup)

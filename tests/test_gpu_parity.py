@@ -328,6 +328,33 @@ def test_gravnet_vs_reference(golden, oracle, red, incl):
     np.testing.assert_allclose(gd, ogd, rtol=1e-6, atol=1e-7)
 
 
+@pytest.mark.parametrize("n,F,k", [(700, 300, 9), (400, 40, 300), (2500, 64, 40)])
+def test_gravnet_wide_and_ordered(oracle, n, F, k):
+    """Several feature chunks (F > 256: float64 grad_d2 partials), k > 255
+    (two-byte arg-max slots), a row visit order, padding and repeated
+    neighbours (one vertex in several slots of a row)."""
+    rng = np.random.default_rng(n + F + k)
+    feats = rng.standard_normal((n, F)).astype(np.float32)
+    idx = rng.integers(0, n, (n, k)).astype(np.int32)
+    idx[:, 0] = np.arange(n)
+    idx[rng.random((n, k)) < 0.1] = -1
+    idx[:, 0] = np.arange(n)
+    d2 = np.where(idx >= 0, rng.random((n, k)) * 0.3, 0).astype(np.float32)
+    d2[:, 0] = 0
+    up = rng.standard_normal((n, 2 * F)).astype(np.float32)
+    order = t(rng.permutation(n).astype(np.int32))
+    spec = fg.AggregationSpec(weight_scale=10.0)
+    nm = fg.NeighborMatrix(t(idx), t(d2))
+    o = oracle.gravnet_aggregate(feats, idx, d2, 10.0)
+    ogf, ogd = oracle.gravnet_aggregate_backward(feats, idx, d2, up, 10.0)
+    for od in (None, order):
+        out = fg.gravnet_aggregate(t(feats), nm, spec, od).cpu().numpy()
+        gf, gd = fg.gravnet_aggregate_backward(t(feats), nm, spec, t(up), od)
+        np.testing.assert_allclose(out, o, rtol=1e-6, atol=1e-7)
+        np.testing.assert_allclose(gf.cpu().numpy(), ogf, rtol=1e-6, atol=1e-6)
+        np.testing.assert_allclose(gd.cpu().numpy(), ogd, rtol=1e-6, atol=1e-6)
+
+
 def test_gravnet_kats():
     # T/test_gravnet.py:40-54, 160-173
     nm = fg.NeighborMatrix(t(np.array([[0, 1], [1, 0]], np.int32)), t(np.array([[0, 1], [0, 1]], np.float32)))
