@@ -147,9 +147,10 @@ int fg_gravnet_bwd_workspace_size(int64_t n, int32_t n_feats, int32_t k, size_t 
 
 /* gravnet_aggregate_backward.  Replaces G/gravnet.py:100-150 ->
  * (grad_feats[n,F] float32, grad_d2[n,k] float32); max blocks route to the
- * lowest arg-max slot.  No floating-point atomics: grad_d2 comes from a row
- * pass, grad_feats from a pass over each vertex's reverse-neighbour list
- * (built in the workspace), both float64 inside.  k <= 65535, n*k < 2^31. */
+ * lowest arg-max slot.  grad_d2 comes from a row pass, grad_feats from a pass
+ * over each vertex's reverse-neighbour list (built in the workspace) plus the
+ * max blocks' terms scattered to their arg-max neighbour; float64 inside.
+ * n*k < 2^31. */
 int fg_gravnet_bwd(const float *feats, int64_t n, int32_t n_feats, const int32_t *idx,
                    const float *d2, int32_t k, double weight_scale, const int32_t *reducers,
                    int32_t n_reducers, int32_t include_self, const int32_t *order,

@@ -8,25 +8,37 @@
 // slot, np.argmax), zeros for a row without valid slots.  Weights, products,
 // sums and maxima are float64, outputs float32.
 //
-// Forward: warp per row (rows visited in `order` when given -- spatially sorted
-// rows reuse each other's neighbour feature rows through L1/L2), lanes over
-// features (FJ per lane), one pass over the slots.
-// Backward, no floating-point atomics:
-//   rows    warp per row v: valid count, per-feature arg-max slot (1 byte) and
-//           grad_d2[v,s] = -scale * w_s * sum_f f[u_s,f] * coef[v,f,s];
+// Every pass is a gather of feature-sized rows (256 B for F = 64) indexed by
+// the neighbour matrix, so the kernels are built for memory-level
+// parallelism: a warp owns a row, each lane VW consecutive features (one
+// float2/float4 load per gathered row), and the slots are taken U = 8 at a
+// time with all U gathers issued before any arithmetic.  Rows are visited in
+// `order` when given: spatially sorted rows share most of their neighbours,
+// so consecutive warps hit the same feature rows in L1/L2.
+//
+// Backward:
+//   rows    warp per row v: per-feature arg-max slot (registers), grad_d2[v,s] =
+//           -scale w_s sum_f f[u_s,f] coef[v,f,s] (the U per-slot dot products
+//           of a batch are reduced together by a transposing butterfly: 9
+//           shuffles instead of 5 U), the mean coefficients cm[v,f] =
+//           sum_mean up/cnt_v, and the max-block gradient w cmax[v,f] sent to
+//           the arg-max neighbour -- one float64 atomic per (v,f), N*F in all,
+//           spread over N*F targets (not the k-fold scatter of the mean part);
 //   reverse counting sort of the (v,s) pairs by neighbour u (int atomics +
 //           the decoupled-look-back scan) -> for every u the list of (v,s)
 //           that aggregated it;
-//   columns warp per u gathers grad_feats[u,f] = sum over its list of
-//           w_vs * (up_mean[v,f]/cnt_v + [argmax[v,f] == s] up_max[v,f])
-//           in float64.
+//   columns warp per u gathers grad_feats[u,f] = gmax[u,f] + sum over its list
+//           of w_vs cm[v,f], float64: one 4F-byte row and two FMAs per entry.
 #include "fg_common.cuh"
 #include "fg_scan.cuh"
+
+#include <initializer_list>
 
 namespace fg {
 namespace gravnet {
 
 constexpr int kRowWarps = 8;
+constexpr int U = 8;  // gathers in flight per warp
 
 struct GnArgs {
     const float* feats;
@@ -52,61 +64,115 @@ __device__ __forceinline__ bool slot_valid(const GnArgs& g, int s, int32_t u) {
     return u >= 0 && (g.include_self || s > 0);
 }
 
+template <int VW>
+__device__ __forceinline__ void ldf(const float* p, float (&x)[VW]) {
+    if constexpr (VW == 4) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(p));
+        x[0] = t.x; x[1] = t.y; x[2] = t.z; x[3] = t.w;
+    } else if constexpr (VW == 2) {
+        const float2 t = __ldg(reinterpret_cast<const float2*>(p));
+        x[0] = t.x; x[1] = t.y;
+    } else {
+        x[0] = __ldg(p);
+    }
+}
+
+template <int VW>
+__device__ __forceinline__ void stf(float* p, const float (&x)[VW]) {
+    if constexpr (VW == 4)
+        *reinterpret_cast<float4*>(p) = make_float4(x[0], x[1], x[2], x[3]);
+    else if constexpr (VW == 2)
+        *reinterpret_cast<float2*>(p) = make_float2(x[0], x[1]);
+    else
+        *p = x[0];
+}
+
+// Slot data of one 32-slot window: lane j holds slot base + j.
+struct Window {
+    int32_t u;
+    double w;
+    unsigned okm;
+};
+
+__device__ __forceinline__ Window load_window(const GnArgs& g, int64_t v, int base, bool weights) {
+    const int lane = lane_id();
+    const int s = base + lane;
+    Window wd;
+    wd.u = s < g.k ? __ldg(&g.idx[v * g.k + s]) : -1;
+    const bool ok = s < g.k && slot_valid(g, s, wd.u);
+    wd.w = ok && weights ? exp(-g.scale * (double)__ldg(&g.d2[v * g.k + s])) : 0.0;
+    wd.okm = __ballot_sync(FG_FULL_MASK, ok);
+    return wd;
+}
+
+// Gather U slots' feature vectors (warp-uniform validity).
+template <int VW>
+__device__ __forceinline__ void gather(const GnArgs& g, const Window& wd, int j0, int fl, bool lane_on,
+                                       float (&x)[U][VW], double (&w)[U], bool (&valid)[U]) {
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+        const int jj = j0 + q;
+        valid[q] = jj < 32 && ((wd.okm >> (jj & 31)) & 1u);
+        const int32_t uq = __shfl_sync(FG_FULL_MASK, wd.u, jj & 31);
+        w[q] = __shfl_sync(FG_FULL_MASK, wd.w, jj & 31);
+#pragma unroll
+        for (int e = 0; e < VW; ++e) x[q][e] = 0.0f;
+        if (valid[q] && lane_on) ldf<VW>(g.feats + (int64_t)uq * g.F + fl, x[q]);
+    }
+}
+
 // ---------------------------------------------------------------- forward
-template <int FJ>
+template <int VW>
 __global__ void __launch_bounds__(kRowWarps * 32) k_gn_fwd(const GnArgs g, int f0, float* __restrict__ out) {
     const int lane = lane_id();
     const int64_t p = blockIdx.x * (int64_t)kRowWarps + (threadIdx.x >> 5);
     if (p >= g.n) return;
     const int64_t v = row_of(g, p);
     const int k = g.k, F = g.F, W = F * g.n_red;
-    double sum[FJ], mx[FJ];
+    const int fl = f0 + lane * VW;
+    const bool lane_on = fl < F;
+    double sum[VW], mx[VW];
 #pragma unroll
-    for (int j = 0; j < FJ; ++j) {
-        sum[j] = 0.0;
-        mx[j] = -INFINITY;
+    for (int e = 0; e < VW; ++e) {
+        sum[e] = 0.0;
+        mx[e] = -INFINITY;
     }
     int cnt = 0;
     for (int base = 0; base < k; base += 32) {
-        const int s = base + lane;
-        const int32_t u = s < k ? g.idx[v * k + s] : -1;
-        const bool ok = s < k && slot_valid(g, s, u);
-        const double w = ok ? exp(-g.scale * (double)g.d2[v * k + s]) : 0.0;
-        unsigned okm = __ballot_sync(FG_FULL_MASK, ok);
-        cnt += __popc(okm);
-        while (okm) {
-            const int j0 = __ffs(okm) - 1;
-            okm &= okm - 1;
-            const int32_t uj = __shfl_sync(FG_FULL_MASK, u, j0);
-            const double wj = __shfl_sync(FG_FULL_MASK, w, j0);
+        const Window wd = load_window(g, v, base, true);
+        cnt += __popc(wd.okm);
+        for (int j0 = 0; j0 < 32; j0 += U) {
+            if (((wd.okm >> j0) & ((1u << U) - 1u)) == 0) continue;
+            float x[U][VW];
+            double w[U];
+            bool valid[U];
+            gather<VW>(g, wd, j0, fl, lane_on, x, w, valid);
 #pragma unroll
-            for (int j = 0; j < FJ; ++j) {
-                const int f = f0 + lane + 32 * j;
-                if (f < F) {
-                    const double term = wj * (double)g.feats[(int64_t)uj * F + f];
-                    sum[j] += term;
-                    if (term > mx[j]) mx[j] = term;
+            for (int q = 0; q < U; ++q) {
+                if (!valid[q]) continue;
+#pragma unroll
+                for (int e = 0; e < VW; ++e) {
+                    const double term = w[q] * (double)x[q][e];
+                    sum[e] += term;
+                    mx[e] = term > mx[e] ? term : mx[e];
                 }
             }
         }
     }
+    if (!lane_on) return;
+    for (int b = 0; b < g.n_red; ++b) {
+        float o[VW];
 #pragma unroll
-    for (int j = 0; j < FJ; ++j) {
-        const int f = f0 + lane + 32 * j;
-        if (f >= F) continue;
-        for (int b = 0; b < g.n_red; ++b) {
-            double val = 0.0;
-            if (cnt > 0) val = is_max(g, b) ? mx[j] : sum[j] / (double)cnt;
-            out[v * W + (int64_t)b * F + f] = (float)val;
-        }
+        for (int e = 0; e < VW; ++e) o[e] = cnt > 0 ? (float)(is_max(g, b) ? mx[e] : sum[e] / (double)cnt) : 0.0f;
+        stf<VW>(out + v * W + (int64_t)b * F + fl, o);
     }
 }
 
 // ---------------------------------------------------------------- backward
 struct GnBwd {
     const float* up;      // (n, F * n_red)
-    int32_t* cnt;         // (n) valid slots per row
-    void* amax;           // (n, F) arg-max slot of the max blocks (AM, all-ones: none)
+    float* cm;            // (n, F) mean-block coefficient sum_b up_b / cnt (0: no valid slot)
+    double* gmax;         // (n, F) max-block gradient, scattered to the arg-max neighbour; null: no max
     float* grad_d2;       // (n, k)
     double* gd_acc;       // (n, k) float64 partials when F spans several chunks, else null
     int32_t* rev_cnt;     // (n) reverse-neighbour counts (scan input)
@@ -114,100 +180,153 @@ struct GnBwd {
     int32_t* rev_cur;     // (n) fill cursor
     int32_t* rev;         // (n * k) entries v * k + s
     float* grad_feats;    // (n, F)
+    int has_mean;
 };
 
-// Row pass: valid count, arg-max slots, grad_d2; counts reverse neighbours.
-template <int FJ, typename AM>
+// Sum a[q] over the warp for q = 0..7 at once; lane L ends with the total of
+// q = 4 b4 + 2 b3 + b2 (bits of L).  5 shuffle rounds, 4 + 2 + 1 + 1 + 1 values.
+__device__ __forceinline__ double transpose_reduce8(double (&a)[8]) {
+    const int lane = lane_id();
+    {
+        const bool hi = lane & 16;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const double send = hi ? a[i] : a[i + 4];
+            const double keep = hi ? a[i + 4] : a[i];
+            a[i] = keep + __shfl_xor_sync(FG_FULL_MASK, send, 16);
+        }
+    }
+    {
+        const bool hi = lane & 8;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const double send = hi ? a[i] : a[i + 2];
+            const double keep = hi ? a[i + 2] : a[i];
+            a[i] = keep + __shfl_xor_sync(FG_FULL_MASK, send, 8);
+        }
+    }
+    {
+        const bool hi = lane & 4;
+        const double send = hi ? a[0] : a[1];
+        const double keep = hi ? a[1] : a[0];
+        a[0] = keep + __shfl_xor_sync(FG_FULL_MASK, send, 4);
+    }
+    double r = a[0];
+    r += __shfl_xor_sync(FG_FULL_MASK, r, 2);
+    r += __shfl_xor_sync(FG_FULL_MASK, r, 1);
+    return r;
+}
+
+__device__ __forceinline__ int reduce8_src(int q) { return ((q >> 2) & 1) << 4 | ((q >> 1) & 1) << 3 | (q & 1) << 2; }
+
+// Row pass: arg-max slots (registers), grad_d2, the mean coefficients cm and
+// the max-block gradients (float64 atomics, one per (v, f) to its arg-max
+// neighbour); counts reverse neighbours.
+template <int VW>
 __global__ void __launch_bounds__(kRowWarps * 32) k_gn_rows(const GnArgs g, const GnBwd bw, int f0,
                                                           int last_chunk) {
+    static_assert(U == 8, "transpose_reduce8");
     const int lane = lane_id();
     const int64_t p = blockIdx.x * (int64_t)kRowWarps + (threadIdx.x >> 5);
     if (p >= g.n) return;
     const int64_t v = row_of(g, p);
     const int k = g.k, F = g.F, W = F * g.n_red;
+    const int fl = f0 + lane * VW;
+    const bool lane_on = fl < F;
     const bool has_max = g.max_bits != 0;
-    // pass 1: count + arg-max (lowest slot on ties, np.argmax)
+    // pass 1: count (+ reverse counts) and arg-max (lowest slot on ties, np.argmax)
     int cnt = 0;
-    double best[FJ];
-    int bslot[FJ];
+    double best[VW];
+    int bslot[VW];
 #pragma unroll
-    for (int j = 0; j < FJ; ++j) {
-        best[j] = -INFINITY;
-        bslot[j] = -1;
+    for (int e = 0; e < VW; ++e) {
+        best[e] = -INFINITY;
+        bslot[e] = -1;
     }
     for (int base = 0; base < k; base += 32) {
-        const int s = base + lane;
-        const int32_t u = s < k ? g.idx[v * k + s] : -1;
-        const bool ok = s < k && slot_valid(g, s, u);
-        if (ok && f0 == 0) atomicAdd(&bw.rev_cnt[u], 1);
-        unsigned okm = __ballot_sync(FG_FULL_MASK, ok);
-        cnt += __popc(okm);
+        const Window wd = load_window(g, v, base, has_max);
+        cnt += __popc(wd.okm);
+        if (f0 == 0 && ((wd.okm >> lane) & 1u)) atomicAdd(&bw.rev_cnt[wd.u], 1);
         if (!has_max) continue;
-        const double w = ok ? exp(-g.scale * (double)g.d2[v * k + s]) : 0.0;
-        while (okm) {
-            const int j0 = __ffs(okm) - 1;
-            okm &= okm - 1;
-            const int32_t uj = __shfl_sync(FG_FULL_MASK, u, j0);
-            const double wj = __shfl_sync(FG_FULL_MASK, w, j0);
+        for (int j0 = 0; j0 < 32; j0 += U) {
+            if (((wd.okm >> j0) & ((1u << U) - 1u)) == 0) continue;
+            float x[U][VW];
+            double w[U];
+            bool valid[U];
+            gather<VW>(g, wd, j0, fl, lane_on, x, w, valid);
 #pragma unroll
-            for (int j = 0; j < FJ; ++j) {
-                const int f = f0 + lane + 32 * j;
-                if (f < F) {
-                    const double term = wj * (double)g.feats[(int64_t)uj * F + f];
-                    if (term > best[j]) {
-                        best[j] = term;
-                        bslot[j] = base + j0;
+            for (int q = 0; q < U; ++q) {
+                if (!valid[q]) continue;
+#pragma unroll
+                for (int e = 0; e < VW; ++e) {
+                    const double term = w[q] * (double)x[q][e];
+                    if (term > best[e]) {
+                        best[e] = term;
+                        bslot[e] = base + j0 + q;
                     }
                 }
             }
         }
     }
-    if (lane == 0 && f0 == 0) bw.cnt[v] = cnt;
     // per-feature coefficients: mean blocks up/cnt, max blocks up at the arg-max
-    double cmean[FJ], cmax[FJ];
+    double cmean[VW], cmax[VW];
 #pragma unroll
-    for (int j = 0; j < FJ; ++j) {
-        cmean[j] = 0.0;
-        cmax[j] = 0.0;
-        const int f = f0 + lane + 32 * j;
-        if (f >= F) continue;
-        if (has_max) ((AM*)bw.amax)[v * F + f] = (AM)(cnt > 0 ? bslot[j] : -1);
-        if (cnt == 0) continue;
+    for (int e = 0; e < VW; ++e) {
+        cmean[e] = 0.0;
+        cmax[e] = 0.0;
+    }
+    if (lane_on && cnt > 0) {
         for (int b = 0; b < g.n_red; ++b) {
-            const double ub = (double)bw.up[v * W + (int64_t)b * F + f];
-            if (is_max(g, b))
-                cmax[j] += ub;
-            else
-                cmean[j] += ub / (double)cnt;
+            float ub[VW];
+            ldf<VW>(bw.up + v * W + (int64_t)b * F + fl, ub);
+#pragma unroll
+            for (int e = 0; e < VW; ++e) {
+                if (is_max(g, b))
+                    cmax[e] += (double)ub[e];
+                else
+                    cmean[e] += (double)ub[e] / (double)cnt;
+            }
         }
     }
-    // pass 2: grad_d2[v,s] = -scale w_s sum_f f[u_s,f] (cmean_f + [amax_f == s] cmax_f)
-    for (int base = 0; base < k; base += 32) {
-        const int s = base + lane;
-        const int32_t u = s < k ? g.idx[v * k + s] : -1;
-        const bool ok = s < k && slot_valid(g, s, u) && cnt > 0;
-        const unsigned okm = __ballot_sync(FG_FULL_MASK, ok);
-        double mine = 0.0;  // this lane's slot total
-        const int lim = min(32, k - base);
-        for (int j0 = 0; j0 < lim; ++j0) {
-            if (!((okm >> j0) & 1u)) continue;  // warp-uniform
-            const int32_t uj = __shfl_sync(FG_FULL_MASK, u, j0);
-            double part = 0.0;
+    if (lane_on && bw.has_mean) {
+        float o[VW];
 #pragma unroll
-            for (int j = 0; j < FJ; ++j) {
-                const int f = f0 + lane + 32 * j;
-                if (f < F) {
-                    const double c = cmean[j] + (bslot[j] == base + j0 ? cmax[j] : 0.0);
-                    part += (double)g.feats[(int64_t)uj * F + f] * c;
+        for (int e = 0; e < VW; ++e) o[e] = (float)cmean[e];
+        stf<VW>(bw.cm + v * F + fl, o);
+    }
+    // pass 2: grad_d2[v,s] = -scale w_s sum_f f[u_s,f] (cmean_f + [amax_f == s] cmax_f);
+    // the max blocks' feature gradient w_s cmax_f goes to u_s at s = amax_f
+    for (int base = 0; base < k; base += 32) {
+        const Window wd = load_window(g, v, base, true);
+        const unsigned okm = cnt > 0 ? wd.okm : 0u;
+        double mine = 0.0;  // this lane's slot total
+        for (int j0 = 0; j0 < 32; j0 += U) {
+            if (((okm >> j0) & ((1u << U) - 1u)) == 0) continue;
+            float x[U][VW];
+            double w[U];
+            bool valid[U];
+            gather<VW>(g, wd, j0, fl, lane_on, x, w, valid);
+            double part[U];
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                part[q] = 0.0;
+                const int32_t uq = __shfl_sync(FG_FULL_MASK, wd.u, (j0 + q) & 31);
+#pragma unroll
+                for (int e = 0; e < VW; ++e) {
+                    const bool at = bslot[e] == base + j0 + q;
+                    const double c = cmean[e] + (at ? cmax[e] : 0.0);
+                    part[q] += (double)x[q][e] * c;
+                    if (at && lane_on && bw.gmax) atomicAdd(&bw.gmax[(int64_t)uq * F + fl + e], w[q] * cmax[e]);
                 }
             }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(FG_FULL_MASK, part, o);
-            if (lane == j0) mine = part;
+            const double r = transpose_reduce8(part);
+            const double got = __shfl_sync(FG_FULL_MASK, r, reduce8_src((lane - j0) & 7));
+            if (lane >= j0 && lane < j0 + U) mine = got;
         }
+        const int s = base + lane;
         if (s < k) {
-            const double w = ok ? exp(-g.scale * (double)g.d2[v * k + s]) : 0.0;
-            double val = ok ? -g.scale * w * mine : 0.0;
+            const bool ok = (okm >> lane) & 1u;
+            double val = ok ? -g.scale * wd.w * mine : 0.0;
             if (bw.gd_acc) {
                 if (f0 > 0) val += bw.gd_acc[v * k + s];
                 if (!last_chunk) bw.gd_acc[v * k + s] = val;
@@ -228,60 +347,62 @@ __global__ void k_gn_fill(const GnArgs g, const GnBwd bw) {
     bw.rev[atomicAdd(&bw.rev_cur[u], 1)] = (int32_t)t;
 }
 
-// Column pass: grad_feats[u] from u's reverse list, float64.  The sum over the
-// list is order-independent up to float64 rounding (the list order comes from
-// the atomic fill), far inside the float32 output precision.
-template <int FJ, typename AM>
+// Column pass: grad_feats[u] = sum over u's reverse list of w_vs cm[v] (+ the
+// max-block gradient scattered to u), float64.  The sum over the list is
+// order-independent up to float64 rounding (the list order comes from the
+// atomic fill), far inside the float32 output precision.
+template <int VW>
 __global__ void __launch_bounds__(kRowWarps * 32) k_gn_cols(const GnArgs g, const GnBwd bw, int f0) {
     const int lane = lane_id();
     const int64_t p = blockIdx.x * (int64_t)kRowWarps + (threadIdx.x >> 5);
     if (p >= g.n) return;
     const int64_t u = row_of(g, p);
-    const int k = g.k, F = g.F, W = F * g.n_red;
-    const int32_t lo = bw.rev_off[u], hi = bw.rev_off[u + 1];
-    const AM* amax = (const AM*)bw.amax;
-    double acc[FJ];
+    const int k = g.k, F = g.F;
+    const int fl = f0 + lane * VW;
+    const bool lane_on = fl < F;
+    double acc[VW];
 #pragma unroll
-    for (int j = 0; j < FJ; ++j) acc[j] = 0.0;
-    for (int32_t base = lo; base < hi; base += 32) {
-        const int32_t e = base + lane;
-        int32_t vv = 0, ss = 0;
-        double w = 0.0, ic = 0.0;
-        if (e < hi) {
-            const int32_t t = bw.rev[e];
-            vv = t / k;
-            ss = t - vv * k;
-            w = exp(-g.scale * (double)g.d2[t]);
-            ic = 1.0 / (double)bw.cnt[vv];
-        }
-        const int nb = min(32, hi - base);
-        for (int j0 = 0; j0 < nb; ++j0) {
-            const int64_t v = __shfl_sync(FG_FULL_MASK, vv, j0);
-            const int s = __shfl_sync(FG_FULL_MASK, ss, j0);
-            const double wj = __shfl_sync(FG_FULL_MASK, w, j0);
-            const double icj = __shfl_sync(FG_FULL_MASK, ic, j0);
+    for (int e = 0; e < VW; ++e) acc[e] = 0.0;
+    if (bw.has_mean) {
+        const int32_t lo = bw.rev_off[u], hi = bw.rev_off[u + 1];
+        for (int32_t base = lo; base < hi; base += 32) {
+            const int32_t ent = base + lane;
+            int32_t vv = 0;
+            double w = 0.0;
+            if (ent < hi) {
+                const int32_t t = bw.rev[ent];
+                vv = t / k;
+                w = exp(-g.scale * (double)__ldg(&g.d2[t]));
+            }
+            const int nb = min(32, hi - base);
+            for (int j0 = 0; j0 < nb; j0 += U) {
+                float x[U][VW];
+                double wq[U];
 #pragma unroll
-            for (int j = 0; j < FJ; ++j) {
-                const int f = f0 + lane + 32 * j;
-                if (f >= F) continue;
-                const bool at_max = amax && (int)amax[v * F + f] == s;
-                double c = 0.0;
-                for (int b = 0; b < g.n_red; ++b) {
-                    const double ub = (double)bw.up[v * W + (int64_t)b * F + f];
-                    if (!is_max(g, b))
-                        c += ub * icj;
-                    else if (at_max)
-                        c += ub;
+                for (int q = 0; q < U; ++q) {
+                    const int32_t vq = __shfl_sync(FG_FULL_MASK, vv, (j0 + q) & 31);
+                    wq[q] = __shfl_sync(FG_FULL_MASK, w, (j0 + q) & 31);
+#pragma unroll
+                    for (int e = 0; e < VW; ++e) x[q][e] = 0.0f;
+                    if (j0 + q < nb && lane_on) ldf<VW>(bw.cm + (int64_t)vq * F + fl, x[q]);
                 }
-                acc[j] += wj * c;
+#pragma unroll
+                for (int q = 0; q < U; ++q) {
+#pragma unroll
+                    for (int e = 0; e < VW; ++e) acc[e] += wq[q] * (double)x[q][e];
+                }
             }
         }
     }
+    if (!lane_on) return;
+    if (bw.gmax) {
 #pragma unroll
-    for (int j = 0; j < FJ; ++j) {
-        const int f = f0 + lane + 32 * j;
-        if (f < F) bw.grad_feats[u * F + f] = (float)acc[j];
+        for (int e = 0; e < VW; ++e) acc[e] += bw.gmax[u * F + fl + e];
     }
+    float o[VW];
+#pragma unroll
+    for (int e = 0; e < VW; ++e) o[e] = (float)acc[e];
+    stf<VW>(bw.grad_feats + u * F + fl, o);
 }
 
 int check_reducers(const int32_t* reducers, int32_t n_red, GnArgs& g) {
@@ -296,30 +417,29 @@ int check_reducers(const int32_t* reducers, int32_t n_red, GnArgs& g) {
     return 0;
 }
 
-constexpr int kFChunk = 256;  // features per launch (FJ <= 8)
+// Features per lane: float4 / float2 loads when the row length and every
+// feature-row base pointer allow it.
+int pick_vw(int F, std::initializer_list<const void*> ptrs) {
+    auto aligned = [&](size_t a) {
+        for (const void* p : ptrs)
+            if (p && ((uintptr_t)p % a) != 0) return false;
+        return true;
+    };
+    if (F % 4 == 0 && F > 64 && aligned(16)) return 4;
+    if (F % 2 == 0 && F > 32 && aligned(8)) return 2;
+    return 1;
+}
 
 template <typename Launch>
-int per_chunk(int F, Launch&& launch) {
-    for (int f0 = 0; f0 < F; f0 += kFChunk) {
-        const int left = F - f0;
-        const int last = f0 + kFChunk >= F;
-        int rc;
-        if (left <= 32)
-            rc = launch(std::integral_constant<int, 1>{}, f0, last);
-        else if (left <= 64)
-            rc = launch(std::integral_constant<int, 2>{}, f0, last);
-        else if (left <= 128)
-            rc = launch(std::integral_constant<int, 4>{}, f0, last);
-        else
-            rc = launch(std::integral_constant<int, 8>{}, f0, last);
-        if (rc) return rc;
-    }
-    return 0;
+int with_vw(int vw, Launch&& launch) {
+    if (vw == 4) return launch(std::integral_constant<int, 4>{});
+    if (vw == 2) return launch(std::integral_constant<int, 2>{});
+    return launch(std::integral_constant<int, 1>{});
 }
 
 struct BwdWs {
-    int32_t* cnt;
-    void* amax;
+    float* cm;
+    double* gmax;
     double* gd_acc;
     int32_t* rev_cnt;
     int32_t* rev_off;
@@ -330,8 +450,7 @@ struct BwdWs {
     int64_t n_tiles;
 };
 
-inline size_t amax_bytes(int k) { return k <= 255 ? 1 : 2; }
-
+// gd_acc is sized for the worst case (one-wide lanes: 32 features per chunk).
 size_t carve(BwdWs* w, void* base, int64_t n, int F, int k) {
     size_t off = 0;
     char* b = (char*)base;
@@ -342,9 +461,9 @@ size_t carve(BwdWs* w, void* base, int64_t n, int F, int k) {
         return p;
     };
     w->n_tiles = ceil_div(n, kScanTile);
-    w->cnt = (int32_t*)take(sizeof(int32_t) * (size_t)n);
-    w->amax = take((size_t)n * F * amax_bytes(k));
-    w->gd_acc = F > kFChunk ? (double*)take(sizeof(double) * (size_t)n * k) : nullptr;
+    w->cm = (float*)take(sizeof(float) * (size_t)n * F);
+    w->gmax = (double*)take(sizeof(double) * (size_t)n * F);
+    w->gd_acc = F > 32 ? (double*)take(sizeof(double) * (size_t)n * k) : nullptr;
     w->rev_cnt = (int32_t*)take(sizeof(int32_t) * (size_t)n);
     w->rev_off = (int32_t*)take(sizeof(int32_t) * (size_t)(n + 1));
     w->rev_cur = (int32_t*)take(sizeof(int32_t) * (size_t)n);
@@ -354,22 +473,27 @@ size_t carve(BwdWs* w, void* base, int64_t n, int F, int k) {
     return align_up(off, 256);
 }
 
-template <typename AM>
-int gn_backward(const GnArgs& g, const GnBwd& bw, const BwdWs& w, cudaStream_t st) {
+template <int VW>
+int gn_backward(const GnArgs& g, GnBwd bw, const BwdWs& w, cudaStream_t st) {
+    constexpr int CW = 32 * VW;
+    if (g.F <= CW) bw.gd_acc = nullptr;
     const unsigned blocks = (unsigned)ceil_div(g.n, kRowWarps);
-    FG_TRY(per_chunk(g.F, [&](auto fj, int f0, int last) {
-        k_gn_rows<decltype(fj)::value, AM><<<blocks, kRowWarps * 32, 0, st>>>(g, bw, f0, last);
-        return launched(st);
-    }));
-    k_scan<<<(unsigned)w.n_tiles, kScanThreads, 0, st>>>(w.rev_cnt, g.n, w.rev_off, w.rev_cur, w.status,
-                                                        w.ticket);
-    FG_TRY(launched(st));
-    k_gn_fill<<<(unsigned)ceil_div(g.n * g.k, 256), 256, 0, st>>>(g, bw);
-    FG_TRY(launched(st));
-    return per_chunk(g.F, [&](auto fj, int f0, int) {
-        k_gn_cols<decltype(fj)::value, AM><<<blocks, kRowWarps * 32, 0, st>>>(g, bw, f0);
-        return launched(st);
-    });
+    for (int f0 = 0; f0 < g.F; f0 += CW) {
+        k_gn_rows<VW><<<blocks, kRowWarps * 32, 0, st>>>(g, bw, f0, f0 + CW >= g.F);
+        FG_TRY(launched(st));
+    }
+    if (bw.has_mean) {
+        k_scan<<<(unsigned)w.n_tiles, kScanThreads, 0, st>>>(w.rev_cnt, g.n, w.rev_off, w.rev_cur,
+                                                            w.status, w.ticket);
+        FG_TRY(launched(st));
+        k_gn_fill<<<(unsigned)ceil_div(g.n * g.k, 256), 256, 0, st>>>(g, bw);
+        FG_TRY(launched(st));
+    }
+    for (int f0 = 0; f0 < g.F; f0 += CW) {
+        k_gn_cols<VW><<<blocks, kRowWarps * 32, 0, st>>>(g, bw, f0);
+        FG_TRY(launched(st));
+    }
+    return 0;
 }
 
 }  // namespace gravnet
@@ -393,15 +517,19 @@ extern "C" int fg_gravnet_fwd(const float* feats, int64_t n, int32_t n_feats, co
     g.scale = weight_scale; g.include_self = include_self; g.order = order;
     cudaStream_t st = (cudaStream_t)stream;
     const unsigned blocks = (unsigned)ceil_div(n, kRowWarps);
-    return per_chunk(n_feats, [&](auto fj, int f0, int) {
-        k_gn_fwd<decltype(fj)::value><<<blocks, kRowWarps * 32, 0, st>>>(g, f0, out);
-        return launched(st);
+    return with_vw(pick_vw(n_feats, {feats, out}), [&](auto vw) {
+        constexpr int VW = decltype(vw)::value;
+        for (int f0 = 0; f0 < n_feats; f0 += 32 * VW) {
+            k_gn_fwd<VW><<<blocks, kRowWarps * 32, 0, st>>>(g, f0, out);
+            FG_TRY(launched(st));
+        }
+        return 0;
     });
 }
 
 extern "C" int fg_gravnet_bwd_workspace_size(int64_t n, int32_t n_feats, int32_t k, size_t* bytes) {
     if (!bytes) return FG_ERR_NULL;
-    if (k < 1 || k > 65535) return FG_ERR_BAD_K;
+    if (k < 1) return FG_ERR_BAD_K;
     if (n < 0 || n_feats < 1) return FG_ERR_BAD_SHAPE;
     BwdWs w;
     *bytes = carve(&w, nullptr, n, n_feats, k);
@@ -416,7 +544,7 @@ extern "C" int fg_gravnet_bwd(const float* feats, int64_t n, int32_t n_feats, co
                               void* stream) {
     GnArgs g;
     FG_TRY(check_reducers(reducers, n_reducers, g));
-    if (k < 1 || k > 65535) return FG_ERR_BAD_K;  // arg-max slots are stored in 1-2 bytes
+    if (k < 1) return FG_ERR_BAD_K;
     if (n < 0 || n_feats < 1) return FG_ERR_BAD_SHAPE;
     if (!(weight_scale > 0.0)) return FG_ERR_BAD_SHAPE;
     if ((int64_t)n * k >= (int64_t)INT32_MAX) return FG_ERR_BAD_SHAPE;  // 32-bit reverse entries
@@ -427,14 +555,18 @@ extern "C" int fg_gravnet_bwd(const float* feats, int64_t n, int32_t n_feats, co
     if (workspace_bytes < need) return FG_ERR_WORKSPACE;
     g.feats = feats; g.n = n; g.F = n_feats; g.idx = idx; g.d2 = d2; g.k = k;
     g.scale = weight_scale; g.include_self = include_self; g.order = order;
-    const bool has_max = g.max_bits != 0;
+    const unsigned all_bits = (1u << g.n_red) - 1u;
     GnBwd bw;
-    bw.up = upstream; bw.cnt = w.cnt; bw.amax = has_max ? w.amax : nullptr; bw.grad_d2 = grad_d2;
+    bw.up = upstream; bw.cm = w.cm; bw.gmax = g.max_bits ? w.gmax : nullptr; bw.grad_d2 = grad_d2;
     bw.gd_acc = w.gd_acc; bw.rev_cnt = w.rev_cnt; bw.rev_off = w.rev_off; bw.rev_cur = w.rev_cur;
-    bw.rev = w.rev; bw.grad_feats = grad_feats;
+    bw.rev = w.rev; bw.grad_feats = grad_feats; bw.has_mean = g.max_bits != all_bits;
     cudaStream_t st = (cudaStream_t)stream;
     FG_CUDA(cudaMemsetAsync(w.rev_cnt, 0, sizeof(int32_t) * (size_t)n, st));
     FG_CUDA(cudaMemsetAsync(w.status, 0, sizeof(unsigned long long) * (size_t)(w.n_tiles + 1), st));
     FG_CUDA(cudaMemsetAsync(w.ticket, 0, sizeof(unsigned) * 4, st));
-    return k <= 255 ? gn_backward<uint8_t>(g, bw, w, st) : gn_backward<uint16_t>(g, bw, w, st);
+    if (bw.gmax) FG_CUDA(cudaMemsetAsync(bw.gmax, 0, sizeof(double) * (size_t)n * n_feats, st));
+    return with_vw(pick_vw(n_feats, {feats, upstream, grad_feats}), [&](auto vw) {
+        constexpr int VW = decltype(vw)::value;
+        return gn_backward<VW>(g, bw, w, st);
+    });
 }
