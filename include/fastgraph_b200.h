@@ -59,6 +59,7 @@ enum fg_status {
 #define FG_KNN_D2_F64 0x8        /* out_d2 is double (bit-exact reference float64 d2);
                                     otherwise float (= float32 of the reference d2)         */
 #define FG_KNN_STATS 0x100       /* diagnostics: count search events (fg_knn_stats)        */
+#define FG_KNN_NO_TILE 0x200     /* diagnostics: skip the lane-per-query tile path         */
 
 /* Reducer codes for the GravNet aggregation (G/gravnet.py:26, order = blocks). */
 #define FG_REDUCE_MEAN 0
@@ -109,9 +110,25 @@ int fg_knn_fwd(const float *sorted_coords, const int32_t *sort_order, const int6
                double max_radius2, uint32_t flags, int32_t *out_idx, void *out_d2,
                void *stream);
 
+/* Scratch bytes fg_knn_fwd_ws needs for this call (0 when only the
+ * warp-per-query kernel runs: d_bin < n_coords, d > 4, k > 41, masks, ...). */
+int fg_knn_workspace_size(int64_t n, int32_t n_coords, int32_t n_splits, int32_t d_bin,
+                          int32_t n_bins, int32_t k, uint32_t flags, size_t *bytes);
+
+/* fg_knn_fwd with caller-owned scratch (no allocation at all).  Same result:
+ * the lane-per-query tile path certifies most rows, the warp-per-query kernel
+ * finishes the rest on the same stream. */
+int fg_knn_fwd_ws(const float *sorted_coords, const int32_t *sort_order, const int64_t *bin_idx,
+                  const int32_t *bin_bounds, const int64_t *row_splits, const double *dim_mins,
+                  const double *widths, int64_t n, int32_t n_coords, int32_t n_splits,
+                  int32_t d_bin, int32_t n_bins, int32_t k, const int8_t *dir_mask,
+                  double max_radius2, uint32_t flags, int32_t *out_idx, void *out_d2,
+                  void *workspace, size_t workspace_bytes, void *stream);
+
 /* Diagnostics: copy (and optionally reset) the counters accumulated by
- * fg_knn_fwd launches made with FG_KNN_STATS: [queries, regions, chunks,
- * appends, compactions, speculative-radius failures, exact epilogues, rows].
+ * fg_knn_fwd launches made with FG_KNN_STATS: warp-per-query kernel [queries,
+ * regions, chunks, appends, compactions, speculative-radius failures, exact
+ * epilogues, rows], then the tile path [tiles, candidates, redo rows, failed tiles].
  * Synchronous; not for the hot path. */
 int fg_knn_stats(uint64_t *out, int32_t n, int32_t reset);
 

@@ -22,6 +22,7 @@ FG_KNN_USE_MAX_R2 = 0x2
 FG_KNN_EXHAUSTIVE = 0x4
 FG_KNN_D2_F64 = 0x8
 FG_KNN_STATS = 0x100
+FG_KNN_NO_TILE = 0x200
 FG_REDUCE_MEAN = 0
 FG_REDUCE_MAX = 1
 
@@ -30,7 +31,7 @@ EXPORTS = (
     "fg_bin_workspace_size", "fg_bin_by_coordinates", "fg_index_replacer", "fg_knn_fwd",
     "fg_knn_bwd_workspace_size", "fg_knn_bwd", "fg_gravnet_fwd",
     "fg_gravnet_bwd_workspace_size", "fg_gravnet_bwd", "fg_error_string", "fg_abi_version",
-    "fg_launch_count", "fg_knn_stats",
+    "fg_launch_count", "fg_knn_stats", "fg_knn_workspace_size", "fg_knn_fwd_ws",
 )
 
 _P = ctypes.c_void_p
@@ -47,6 +48,9 @@ _SIGS = {
     "fg_index_replacer": ([_P, _I64, _P, _I64, _P], ctypes.c_int),
     "fg_knn_fwd": ([_P, _P, _P, _P, _P, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _P, _D, _U32,
                     _P, _P, _P], ctypes.c_int),
+    "fg_knn_workspace_size": ([_I64, _I32, _I32, _I32, _I32, _I32, _U32, _SZ], ctypes.c_int),
+    "fg_knn_fwd_ws": ([_P, _P, _P, _P, _P, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _P, _D,
+                       _U32, _P, _P, _P, ctypes.c_size_t, _P], ctypes.c_int),
     "fg_knn_bwd_workspace_size": ([_I64, _I32, _SZ], ctypes.c_int),
     "fg_knn_bwd": ([_P, _I64, _I32, _P, _I32, _P, _P, _P, _I32, _P, ctypes.c_size_t, _P],
                    ctypes.c_int),

@@ -1,22 +1,37 @@
 // fg_knn.cu -- C ABI entry of binned_select_knn forward (kernels: fg_knn_impl.cuh).
 #include <mutex>
 
-#include "fg_knn_impl.cuh"
+#include "fg_knn_tile.cuh"
 
 using namespace fg;
 using namespace fg::search;
 
+namespace fg {
+namespace tile {
+int launch(TileArgs& t, const search::KnnArgs& a, int d_bin, cudaStream_t st);
+}
+}  // namespace fg
+
 namespace {
 unsigned long long* g_stats_dev = nullptr;  // FG_KNN_STATS counters (lazily allocated)
 std::mutex g_stats_mu;
-}  // namespace
+constexpr int kStatsTotal = ST_COUNT + tile::TS_COUNT;
 
-extern "C" int fg_knn_fwd(const float* sorted_coords, const int32_t* sort_order,
-                          const int64_t* bin_idx, const int32_t* bin_bounds,
-                          const int64_t* row_splits, const double* dim_mins, const double* widths,
-                          int64_t n, int32_t n_coords, int32_t n_splits, int32_t d_bin,
-                          int32_t n_bins, int32_t k, const int8_t* dir_mask, double max_radius2,
-                          uint32_t flags, int32_t* out_idx, void* out_d2, void* stream) {
+// The lane-per-query tile path (fg_knn_tile.cuh) serves every coordinate
+// binned, d <= 4, k - 1 <= 40, no mask / radius / exhaustive / float64 output.
+bool tile_path(int32_t n_coords, int32_t d_bin, int32_t n_bins, int32_t k, uint32_t flags) {
+    const uint32_t off = FG_KNN_USE_DIRECTION | FG_KNN_USE_MAX_R2 | FG_KNN_EXHAUSTIVE |
+                         FG_KNN_D2_F64 | FG_KNN_NO_TILE;
+    return n_coords == d_bin && n_coords <= 4 && n_bins <= 32 && k >= 2 &&
+           k - 1 <= tile::kMaxNeed && !(flags & off);
+}
+
+// Argument validation shared by both entry points (before any CUDA call).
+int check_args(const float* sorted_coords, const int32_t* sort_order, const int64_t* bin_idx,
+               const int32_t* bin_bounds, const int64_t* row_splits, const double* dim_mins,
+               const double* widths, int64_t n, int32_t n_coords, int32_t n_splits, int32_t d_bin,
+               int32_t n_bins, int32_t k, const int8_t* dir_mask, double max_radius2,
+               uint32_t flags, const int32_t* out_idx, const void* out_d2) {
     if (k < 1 || k > 960) return FG_ERR_BAD_K;
     if (n < 0 || n >= ((int64_t)1 << 31) || n_splits < 1 || n_bins < 1) return FG_ERR_BAD_SHAPE;
     if (n_coords < 1) return FG_ERR_BAD_SHAPE;
@@ -31,6 +46,84 @@ extern "C" int fg_knn_fwd(const float* sorted_coords, const int32_t* sort_order,
         !widths || !out_idx || !out_d2)
         return FG_ERR_NULL;
     if ((flags & FG_KNN_USE_DIRECTION) && !dir_mask) return FG_ERR_NULL;
+    return 0;
+}
+
+struct TileWs {
+    int* ctr;
+    int2* tiles;
+    int32_t* redo;
+    size_t bytes;
+    int64_t n_blocks;
+};
+
+TileWs tile_ws(void* base, int64_t n, int32_t n_splits, int32_t d_bin, int32_t n_bins) {
+    TileWs w;
+    const int64_t nblk = (n_bins + 1) / 2;
+    int64_t bps = 1;
+    for (int i = 0; i < d_bin - 1; ++i) bps *= nblk;
+    w.n_blocks = bps * n_splits;
+    const int64_t max_tiles = w.n_blocks * n_bins;
+    char* p = static_cast<char*>(base);
+    size_t off = 0;
+    w.ctr = reinterpret_cast<int*>(p + off);
+    off += 64;
+    w.tiles = reinterpret_cast<int2*>(p + off);
+    off = align_up(off + sizeof(int2) * (size_t)max_tiles, 256);
+    w.redo = reinterpret_cast<int32_t*>(p + off);
+    off = align_up(off + sizeof(int32_t) * (size_t)std::max<int64_t>(n, 1), 256);
+    w.bytes = off;
+    return w;
+}
+}  // namespace
+
+extern "C" int fg_knn_workspace_size(int64_t n, int32_t n_coords, int32_t n_splits, int32_t d_bin,
+                                     int32_t n_bins, int32_t k, uint32_t flags, size_t* bytes) {
+    if (!bytes) return FG_ERR_NULL;
+    if (n < 0 || n_splits < 1 || n_bins < 1) return FG_ERR_BAD_SHAPE;
+    *bytes = tile_path(n_coords, d_bin, n_bins, k, flags)
+                 ? tile_ws(nullptr, n, n_splits, d_bin, n_bins).bytes
+                 : 0;
+    return 0;
+}
+
+extern "C" int fg_knn_fwd(const float* sorted_coords, const int32_t* sort_order,
+                          const int64_t* bin_idx, const int32_t* bin_bounds,
+                          const int64_t* row_splits, const double* dim_mins, const double* widths,
+                          int64_t n, int32_t n_coords, int32_t n_splits, int32_t d_bin,
+                          int32_t n_bins, int32_t k, const int8_t* dir_mask, double max_radius2,
+                          uint32_t flags, int32_t* out_idx, void* out_d2, void* stream) {
+    // convenience entry: stream-ordered scratch from the CUDA memory pool
+    FG_TRY(check_args(sorted_coords, sort_order, bin_idx, bin_bounds, row_splits, dim_mins, widths,
+                      n, n_coords, n_splits, d_bin, n_bins, k, dir_mask, max_radius2, flags,
+                      out_idx, out_d2));
+    if (n == 0) return 0;
+    size_t bytes = 0;
+    if (tile_path(n_coords, d_bin, n_bins, k, flags))
+        bytes = tile_ws(nullptr, n, n_splits, d_bin, n_bins).bytes;
+    void* ws = nullptr;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (bytes) FG_CUDA(cudaMallocAsync(&ws, bytes, st));
+    const int rc = fg_knn_fwd_ws(sorted_coords, sort_order, bin_idx, bin_bounds, row_splits,
+                                 dim_mins, widths, n, n_coords, n_splits, d_bin, n_bins, k,
+                                 dir_mask, max_radius2, flags, out_idx, out_d2, ws, bytes, stream);
+    if (ws) FG_CUDA(cudaFreeAsync(ws, st));
+    return rc;
+}
+
+extern "C" int fg_knn_fwd_ws(const float* sorted_coords, const int32_t* sort_order,
+                             const int64_t* bin_idx, const int32_t* bin_bounds,
+                             const int64_t* row_splits, const double* dim_mins,
+                             const double* widths, int64_t n, int32_t n_coords, int32_t n_splits,
+                             int32_t d_bin, int32_t n_bins, int32_t k, const int8_t* dir_mask,
+                             double max_radius2, uint32_t flags, int32_t* out_idx, void* out_d2,
+                             void* workspace, size_t workspace_bytes, void* stream) {
+    FG_TRY(check_args(sorted_coords, sort_order, bin_idx, bin_bounds, row_splits, dim_mins, widths,
+                      n, n_coords, n_splits, d_bin, n_bins, k, dir_mask, max_radius2, flags,
+                      out_idx, out_d2));
+    if (n == 0) return 0;
+    int64_t total = 1;
+    for (int i = 0; i < d_bin; ++i) total *= n_bins;
     KnnArgs a;
     a.sc = reinterpret_cast<const float4*>(sorted_coords);
     a.sid = sort_order;
@@ -51,15 +144,41 @@ extern "C" int fg_knn_fwd(const float* sorted_coords, const int32_t* sort_order,
     a.out_idx = out_idx;
     a.out_d2 = out_d2;
     a.stats = nullptr;
+    a.qlist = nullptr;
+    a.qcount = nullptr;
     if (flags & FG_KNN_STATS) {
         std::lock_guard<std::mutex> lk(g_stats_mu);
         if (!g_stats_dev) {
-            FG_CUDA(cudaMalloc(&g_stats_dev, sizeof(unsigned long long) * ST_COUNT));
-            FG_CUDA(cudaMemset(g_stats_dev, 0, sizeof(unsigned long long) * ST_COUNT));
+            FG_CUDA(cudaMalloc(&g_stats_dev, sizeof(unsigned long long) * kStatsTotal));
+            FG_CUDA(cudaMemset(g_stats_dev, 0, sizeof(unsigned long long) * kStatsTotal));
         }
         a.stats = g_stats_dev;
     }
     cudaStream_t st = (cudaStream_t)stream;
+    if (tile_path(n_coords, d_bin, n_bins, k, flags)) {
+        const TileWs w = tile_ws(workspace, n, n_splits, d_bin, n_bins);
+        if (!workspace) return FG_ERR_NULL;
+        if (workspace_bytes < w.bytes) return FG_ERR_WORKSPACE;
+        tile::TileArgs t;
+        t.sc = a.sc;
+        t.sid = sort_order;
+        t.bounds = bin_bounds;
+        t.mins = dim_mins;
+        t.widths = widths;
+        t.total = total;
+        t.nb = n_bins;
+        t.k = k;
+        t.nblk = (n_bins + 1) / 2;
+        t.bps = (int)(w.n_blocks / n_splits);
+        t.n_blocks = (int)w.n_blocks;
+        t.tiles = w.tiles;
+        t.ctr = w.ctr;
+        t.redo = w.redo;
+        t.out_idx = out_idx;
+        t.out_d2 = reinterpret_cast<float*>(out_d2);
+        t.stats = a.stats ? a.stats + ST_COUNT : nullptr;
+        return tile::launch(t, a, d_bin, st);
+    }
     switch ((n_coords + 3) / 4) {
         case 1: return dispatch_nv1(a, d_bin, st);
         case 2: return dispatch_nv2(a, d_bin, st);
@@ -70,11 +189,11 @@ extern "C" int fg_knn_fwd(const float* sorted_coords, const int32_t* sort_order,
 
 extern "C" int fg_knn_stats(uint64_t* out, int32_t n, int32_t reset) {
     std::lock_guard<std::mutex> lk(g_stats_mu);
-    unsigned long long h[ST_COUNT] = {0};
+    unsigned long long h[kStatsTotal] = {0};
     if (g_stats_dev) {
         FG_CUDA(cudaMemcpy(h, g_stats_dev, sizeof(h), cudaMemcpyDeviceToHost));
         if (reset) FG_CUDA(cudaMemset(g_stats_dev, 0, sizeof(h)));
     }
-    for (int i = 0; i < n && i < ST_COUNT; ++i) out[i] = h[i];
+    for (int i = 0; i < n && i < kStatsTotal; ++i) out[i] = h[i];
     return 0;
 }

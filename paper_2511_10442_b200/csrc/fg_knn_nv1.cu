@@ -1,8 +1,44 @@
-// Search kernels for coordinates of 1..4 dims (NV = 1 float4 per point).
-#include "fg_knn_impl.cuh"
+// Search kernels for coordinates of 1..4 dims (NV = 1 float4 per point):
+// the warp-per-query kernel and the lane-per-query tile path.
+#include "fg_knn_tile.cuh"
 
 namespace fg {
 namespace search {
 int dispatch_nv1(const KnnArgs& a, int d_bin, cudaStream_t st) { return dispatch_db<1>(a, d_bin, st); }
 }  // namespace search
+
+namespace tile {
+
+template <int DB>
+int launch_db(TileArgs& t, const search::KnnArgs& a, cudaStream_t st) {
+    FG_CUDA(cudaMemsetAsync(t.ctr, 0, 4 * sizeof(int), st));
+    k_tiles<DB><<<(unsigned)ceil_div(t.n_blocks, 4), 128, 0, st>>>(t);
+    FG_TRY(launched(st));
+    static int sms = 0;  // per template instance: also sets the smem opt-in once
+    if (!sms) {
+        int dev = 0;
+        FG_CUDA(cudaGetDevice(&dev));
+        FG_CUDA(cudaFuncSetAttribute(k_tile_search<DB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)tile_smem_bytes()));
+        FG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    k_tile_search<DB><<<(unsigned)(sms * 2), kWarps * 32, tile_smem_bytes(), st>>>(t);
+    FG_TRY(launched(st));
+    // whatever the tiles could not certify: the warp-per-query kernel
+    search::KnnArgs r = a;
+    r.qlist = t.redo;
+    r.qcount = &t.ctr[2];
+    return search::dispatch_db<1>(r, DB, st);
+}
+
+int launch(TileArgs& t, const search::KnnArgs& a, int d_bin, cudaStream_t st) {
+    switch (d_bin) {
+        case 1: return launch_db<1>(t, a, st);
+        case 2: return launch_db<2>(t, a, st);
+        case 3: return launch_db<3>(t, a, st);
+        default: return launch_db<4>(t, a, st);
+    }
+}
+
+}  // namespace tile
 }  // namespace fg

@@ -49,7 +49,7 @@ def set_debug_flags(flags: int) -> None:
 
 def knn_stats(reset: bool = True) -> dict:
     names = ("queries", "regions", "chunks", "appends", "compactions", "spec_fail", "exact_epi",
-             "rows")
+             "rows", "tiles", "tile_candidates", "tile_redo", "tile_fail")
     buf = (ctypes.c_uint64 * len(names))()
     _lib.check(_lib.load().fg_knn_stats(ctypes.cast(buf, ctypes.c_void_p), len(names), int(reset)))
     return dict(zip(names, [int(x) for x in buf]))
@@ -175,10 +175,12 @@ def binned_select_knn(coords: Tensor, row_splits: Tensor, bin_idx: Tensor, sort_
     flags |= _DEBUG_FLAGS
     idx = torch.empty((n, K), dtype=torch.int32, device=dev)
     d2 = torch.empty((n, K), dtype=torch.float64 if d2_f64 else torch.float32, device=dev)
-    _lib.check(L.fg_knn_fwd(_p(sorted_coords), _p(sort_order), _p(bin_idx), _p(bin_bounds), _p(rs),
-                            _p(dim_mins), _p(widths), n, n_c, S, d_bin, n_bins, K, _p(dir_t),
-                            float(max_radius2 or 0.0), flags, _p(idx), _p(d2),
-                            _stream(sorted_coords)), "binned_select_knn")
+    nbytes = _lib.size_out(L.fg_knn_workspace_size, n, n_c, S, d_bin, n_bins, K, flags)
+    ws = _ws(nbytes, dev)
+    _lib.check(L.fg_knn_fwd_ws(_p(sorted_coords), _p(sort_order), _p(bin_idx), _p(bin_bounds),
+                               _p(rs), _p(dim_mins), _p(widths), n, n_c, S, d_bin, n_bins, K,
+                               _p(dir_t), float(max_radius2 or 0.0), flags, _p(idx), _p(d2),
+                               _p(ws), ws.numel(), _stream(sorted_coords)), "binned_select_knn")
     return idx, d2
 
 

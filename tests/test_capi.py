@@ -61,6 +61,16 @@ def test_validation_before_launch():
     assert knn(n_c=17) == -6              # too many dims
     assert knn(r2=-1.0, flags=0x2) == -7  # negative radius
     assert knn() == -5                    # NULL pointers
+    def knn_ws(ws_bytes, n=10, n_c=4, k=5):
+        return L.fg_knn_fwd_ws(None, None, None, None, None, None, None, n, n_c, 1, 4, 5, k,
+                               None, 0.0, 0, None, None, None, ws_bytes, None)
+    assert knn_ws(0, k=0) == -1
+    assert knn_ws(0) == -5
+    # the tile path needs scratch; the warp-per-query path (here d_bin < n_c) needs none
+    assert L.fg_knn_workspace_size(1000, 4, 1, 4, 29, 40, 0, ctypes.byref(n)) == 0 and n.value > 4000
+    assert L.fg_knn_workspace_size(1000, 5, 1, 4, 29, 40, 0, ctypes.byref(n)) == 0 and n.value == 0
+    assert L.fg_knn_workspace_size(1000, 4, 1, 4, 29, 40, _lib.FG_KNN_NO_TILE,
+                                   ctypes.byref(n)) == 0 and n.value == 0
     for rc, exc in ((-1, errors.BadKError), (-3, errors.TooFewDimsError),
                     (-6, errors.BadShapeError), (-7, errors.BadKError)):
         with pytest.raises(exc):

@@ -1,0 +1,89 @@
+"""GPU parity of the lane-per-query tile path (csrc/fg_knn_tile.cuh).
+
+The tile path serves float32-distance searches with every coordinate binned
+(d <= 4, k <= 41, no mask / radius / exhaustive); whatever it cannot certify
+goes to the warp-per-query kernel.  Both must give the canonical answer
+(float64 d2 in the reference's operation order, lower index wins ties), so:
+small cases against the CPU oracle bit for bit, full BASELINE sizes against the
+warp-per-query kernel bit for bit (FG_KNN_NO_TILE), plus the redo fraction the
+design promises on uniform data.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+import paper_2511_10442_b200 as fg  # noqa: E402
+from paper_2511_10442_b200 import _lib, ops  # noqa: E402
+from paper_2511_10442_b200.datasets import config_dataset, generate_dataset  # noqa: E402
+
+
+def search(c32, off, k, flags=0, stats=False):
+    n, d = c32.shape
+    sizes = np.diff(off)
+    nb = fg.compute_n_bins(int(sizes.max()), k, d)
+    ct = torch.from_numpy(np.ascontiguousarray(c32)).cuda()
+    rs = torch.from_numpy(np.asarray(off, np.int64)).cuda()
+    bi, so, bb, mi, wi, sc = ops.bin_by_coordinates(ct, rs, d, nb)
+    ops.set_debug_flags(flags | (_lib.FG_KNN_STATS if stats else 0))
+    try:
+        if stats:
+            ops.knn_stats(reset=True)
+        idx, d2 = ops.binned_select_knn(ct, rs, bi, so, bb, mi, wi, sc, k, d, nb, None, None,
+                                        False, False)
+        torch.cuda.synchronize()
+        st = ops.knn_stats(reset=True) if stats else None
+    finally:
+        ops.set_debug_flags(0)
+    return idx.cpu().numpy(), d2.cpu().numpy(), st
+
+
+def assert_oracle(O, c32, off, k):
+    oi, od = O.knn_canonical(c32.astype(np.float64), np.asarray(off, np.int64), k)
+    gi, gd, st = search(c32, off, k, stats=True)
+    bad = np.nonzero(~((gi == oi).all(1) & (gd == od.astype(np.float32)).all(1)))[0]
+    assert bad.size == 0, (f"{bad.size} rows differ; first {bad[:3]}: gpu {gi[bad[0]]} "
+                           f"oracle {oi[bad[0]]}")
+    return st
+
+
+@pytest.mark.parametrize("d,k,S,seed", [(4, 40, 1, 0), (4, 41, 2, 1), (4, 2, 1, 2), (3, 16, 3, 3),
+                                        (3, 33, 1, 4), (2, 12, 2, 5), (2, 40, 1, 6), (1, 9, 1, 7),
+                                        (4, 24, 4, 8)])
+def test_tile_vs_oracle_uniform(oracle, d, k, S, seed):
+    c, off = generate_dataset(12_000, d, S, seed, "uniform")
+    st = assert_oracle(oracle, c.astype(np.float32), off, k)
+    assert st["tiles"] > 0  # the tile path actually ran
+
+
+def test_tile_ties_and_duplicates(oracle):
+    # integer lattice: exact distance ties everywhere (tie rows go to the exact path)
+    g = np.stack(np.meshgrid(*[np.arange(12)] * 4, indexing="ij"), -1).reshape(-1, 4)
+    g = g[np.random.default_rng(0).permutation(len(g))].astype(np.float32)
+    assert_oracle(oracle, g, [0, len(g)], 20)
+    # coincident piles inside uniform background
+    rng = np.random.default_rng(3)
+    c = np.concatenate([np.full((500, 4), 0.5), rng.random((8000, 4)),
+                        np.full((40, 4), 0.25)]).astype(np.float32)
+    c = c[rng.permutation(len(c))]
+    assert_oracle(oracle, c, [0, len(c)], 40)
+
+
+def test_tile_clusters_and_tiny_splits(oracle):
+    c, off = generate_dataset(20_000, 4, 2, 9, "clusters")
+    assert_oracle(oracle, c.astype(np.float32), off, 40)
+    c = np.random.default_rng(5).random((900, 4)).astype(np.float32)
+    assert_oracle(oracle, c, np.array([0, 30, 30, 41, 900]), 40)  # splits smaller than k
+
+
+@pytest.mark.parametrize("cfg", ["north_star", "E", "A"])
+def test_tile_equals_warp_kernel_full_size(cfg):
+    c, off, k = config_dataset(cfg)
+    i0, d0, _ = search(c, off, k, flags=_lib.FG_KNN_NO_TILE)
+    i1, d1, st = search(c, off, k, stats=True)
+    assert np.array_equal(i0, i1)
+    assert np.array_equal(d0.view(np.uint32), d1.view(np.uint32))
+    if cfg != "A":  # uniform 1M / 500k: the tile path certifies >= 99.5% of rows
+        assert st["tile_redo"] < 0.005 * len(c), st
