@@ -45,12 +45,12 @@
 namespace fg {
 namespace tile {
 
-constexpr int kWarps = 4;          // warps per CTA
+constexpr int kWarps = 4;          // warps per CTA (4 CTAs per SM: 16 warps)
 constexpr int kCap = 88;           // list entries per lane
 constexpr int kSlack = 32;         // one chunk of overrun before the clamp
-constexpr int kBkt = 32;           // epilogue buckets
-constexpr int kHistStride = kBkt + 4;  // bytes per lane (bank spread)
-constexpr int kMaxSpans = 384;     // candidate spans per tile
+constexpr int kStride = kCap + kSlack + 2;  // u16 per lane list: 61 words, odd -> bank spread
+constexpr int kBkt = 64;           // epilogue buckets (2 per lane)
+constexpr int kMaxSpans = 320;     // candidate spans per tile
 constexpr int kMaxSpanLen = 127;   // 7-bit offsets in the codes
 constexpr float kAlpha = 1.12f;    // radius inflation over the density estimate
 constexpr float kMargin = 1.0f + 1e-5f;
@@ -58,7 +58,7 @@ constexpr float kSlackCells = 1e-4f;
 constexpr float kInf = __builtin_huge_valf();
 constexpr int kMaxNeed = 40;       // host eligibility: k - 1 <= kMaxNeed
 
-enum { TS_TILES, TS_CAND, TS_REDO, TS_TILE_FAIL, TS_COUNT };
+enum { TS_TILES, TS_CAND, TS_REDO, TS_TILE_FAIL, TS_EXPANDED, TS_COUNT };
 
 struct TileArgs {
     const float4* sc;
@@ -79,13 +79,14 @@ struct TileArgs {
 };
 
 struct TileWarp {
-    uint16_t code[(kCap + kSlack) * 32];  // [slot][lane] list entries
-    float key[kCap * 32];                 // [slot][lane] epilogue keys
-    uint8_t order[kCap * 32];             // [slot][lane] bucket-sorted entries
-    uint8_t hist[32 * kHistStride];       // [lane][bucket]
+    uint16_t code[32 * kStride];          // [lane][slot] per-lane candidate lists
+    float skey[kCap];                     // epilogue staging of one query: keys
+    uint16_t scd[kCap];                   //   and codes, in (bucket, key) order
+    uint32_t bcnt[kBkt];                  //   bucket counts -> starts
     int32_t spS[kMaxSpans];               // span start (sorted position)
     uint16_t spE[kMaxSpans + 1];          // span flattened start (exclusive prefix)
-    alignas(16) float sx[4][32];          // chunk coordinates, SoA
+    alignas(16) float sx[4][32];          // chunk coordinates, SoA (centred in expanded mode)
+    alignas(16) float sn[32];             // expanded mode: |c - centre|^2
     alignas(16) uint32_t scode[32];       // chunk codes
 };
 
@@ -223,9 +224,172 @@ __device__ __forceinline__ void eval_g4(const G4& g, const QP& q, float tau, uin
     for (int i = 0; i < 4; ++i)
         asm volatile(
             "{ .reg .pred p; setp.le.f32 p, %1, %2; @p st.shared.u16 [%0], %3; "
-            "@p add.u32 %0, %0, 64; }"
+            "@p add.u32 %0, %0, 2; }"
             : "+r"(ptr)
             : "f"(d[i]), "f"(tau), "r"(cs[i]));
+}
+
+// Expanded form around the tile centre: d2 = |q'|^2 + |c'|^2 - 2 q'.c' with
+// q' = q - centre, c' = c - centre (FADD2 + 4 FFMA2 per candidate pair).  Used
+// only when its rounding error, <= 12u (|q'| + |c'|)^2 + 2u (|q'| + |c'|) |q-c|,
+// stays below 2.5e-5 tau of every lane (checked per tile); else the direct form.
+struct QX {
+    unsigned long long sq;      // (|q'|^2, |q'|^2)
+    unsigned long long m2q[4];  // (-2 q'_d, -2 q'_d)
+};
+struct G4X {
+    unsigned long long x[4][2];
+    unsigned long long n[2];
+};
+__device__ __forceinline__ void load_g4x(G4X& g, uint32_t sx_addr, int j) {
+#pragma unroll
+    for (int d = 0; d < 4; ++d)
+        asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];"
+                     : "=l"(g.x[d][0]), "=l"(g.x[d][1])
+                     : "r"(sx_addr + d * 128 + j * 4));
+    asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];"
+                 : "=l"(g.n[0]), "=l"(g.n[1])
+                 : "r"(sx_addr + 4 * 128 + j * 4));
+}
+__device__ __forceinline__ void eval_g4x(const G4X& g, const QX& q, float tau, uint32_t& ptr,
+                                         uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3) {
+    float d[4];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        unsigned long long acc;
+        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc) : "l"(g.n[h]), "l"(q.sq));
+#pragma unroll
+        for (int dd = 0; dd < 4; ++dd)
+            asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(acc) : "l"(g.x[dd][h]), "l"(q.m2q[dd]), "l"(acc));
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(d[2 * h]), "=f"(d[2 * h + 1]) : "l"(acc));
+    }
+    const uint32_t cs[4] = {c0, c1, c2, c3};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        asm volatile(
+            "{ .reg .pred p; setp.le.f32 p, %1, %2; @p st.shared.u16 [%0], %3; "
+            "@p add.u32 %0, %0, 2; }"
+            : "+r"(ptr)
+            : "f"(d[i]), "f"(tau), "r"(cs[i]));
+}
+
+__device__ __forceinline__ void eval_g8x(const G4X& g0, const G4X& g1, const QX& q, float tau,
+                                         uint32_t& ptr, const uint32_t* cs) {
+    float d[8];
+    unsigned long long acc[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+        const G4X& g = h < 2 ? g0 : g1;
+        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc[h]) : "l"(g.n[h & 1]), "l"(q.sq));
+    }
+#pragma unroll
+    for (int dd = 0; dd < 4; ++dd)
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const G4X& g = h < 2 ? g0 : g1;
+            asm("fma.rn.f32x2 %0, %1, %2, %3;"
+                : "=l"(acc[h]) : "l"(g.x[dd][h & 1]), "l"(q.m2q[dd]), "l"(acc[h]));
+        }
+#pragma unroll
+    for (int h = 0; h < 4; ++h)
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(d[2 * h]), "=f"(d[2 * h + 1]) : "l"(acc[h]));
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        asm volatile(
+            "{ .reg .pred p; setp.le.f32 p, %1, %2; @p st.shared.u16 [%0], %3; "
+            "@p add.u32 %0, %0, 2; }"
+            : "+r"(ptr)
+            : "f"(d[i]), "f"(tau), "r"(cs[i]));
+}
+
+__device__ __forceinline__ unsigned long long pack2(float x) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(x));
+    return r;
+}
+
+// Stream the tile's candidates in 32-candidate chunks (coalesced loads into
+// shared memory, then broadcast) and append each lane's passing codes.
+template <bool EXP>
+__device__ __forceinline__ void scan_tile(TileWarp& W, const float4* __restrict__ sc, int T, int nsp,
+                                          const QP& qv, const QX& qx, const float4 cen, float tau,
+                                          uint32_t& ptr, bool& overflow, uint32_t llim) {
+    const int lane = lane_id();
+    const uint32_t sx_addr = (uint32_t)__cvta_generic_to_shared(&W.sx[0][0]);
+    // chunk c+1's candidate is loaded (global) while chunk c is evaluated
+    int s0 = 0;
+    auto fetch = [&](int f0, float4& c, uint32_t& code, bool& live) {
+        const int f = f0 + lane;
+        const int si = s0 + lane;
+        const int st = si < nsp ? W.spE[si] : 0x7fffffff;
+        const unsigned starts = __reduce_or_sync(
+            FG_FULL_MASK, (lane > 0 && st > f0 && st < f0 + 32) ? 1u << (st - f0) : 0u);
+        const int g = s0 + __popc(starts & ((2u << lane) - 1u));
+        live = f < T;
+        code = 0;
+        if (live) {
+            const int off = f - W.spE[g];
+            c = sc[W.spS[g] + off];
+            code = (uint32_t)((g << 7) | off);
+        }
+        s0 = __shfl_sync(FG_FULL_MASK, g, 31);
+        if (s0 + 1 < nsp && W.spE[s0 + 1] == f0 + 32) ++s0;
+    };
+    float4 cn = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t coden = 0;
+    bool liven = false;
+    if (T > 0) fetch(0, cn, coden, liven);
+    for (int f0 = 0; f0 < T; f0 += 32) {
+        float4 c = cn;
+        const uint32_t code = coden;
+        const bool live = liven;
+        if (f0 + 32 < T) fetch(f0 + 32, cn, coden, liven);
+        float nn = kInf;
+        if (!live) {
+            c = EXP ? make_float4(0.f, 0.f, 0.f, 0.f) : make_float4(kInf, kInf, kInf, kInf);
+        } else if (EXP) {
+            c.x -= cen.x; c.y -= cen.y; c.z -= cen.z; c.w -= cen.w;
+            nn = fmaf(c.w, c.w, fmaf(c.z, c.z, fmaf(c.y, c.y, c.x * c.x)));
+        }
+        W.sx[0][lane] = c.x;
+        W.sx[1][lane] = c.y;
+        W.sx[2][lane] = c.z;
+        W.sx[3][lane] = c.w;
+        if (EXP) W.sn[lane] = nn;
+        W.scode[lane] = code;
+        __syncwarp();
+        uint32_t cd[32];  // the chunk's codes (uniform), in registers
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint4 v = reinterpret_cast<const uint4*>(W.scode)[j];
+            cd[4 * j] = v.x; cd[4 * j + 1] = v.y; cd[4 * j + 2] = v.z; cd[4 * j + 3] = v.w;
+        }
+        // software pipeline: the next group's loads precede this group's stores
+        if (EXP) {
+            G4X gb[2];
+            load_g4x(gb[0], sx_addr, 0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (j + 1 < 8) load_g4x(gb[(j + 1) & 1], sx_addr, 4 * (j + 1));
+                eval_g4x(gb[j & 1], qx, tau, ptr, cd[4 * j], cd[4 * j + 1], cd[4 * j + 2],
+                         cd[4 * j + 3]);
+            }
+        } else {
+            G4 gb[2];
+            load_g4(gb[0], sx_addr, 0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (j + 1 < 8) load_g4(gb[(j + 1) & 1], sx_addr, 4 * (j + 1));
+                eval_g4(gb[j & 1], qv, tau, ptr, cd[4 * j], cd[4 * j + 1], cd[4 * j + 2],
+                        cd[4 * j + 3]);
+            }
+        }
+        if (ptr > llim) {
+            overflow = true;
+            ptr = llim;
+        }
+        __syncwarp();
+    }
 }
 
 // fp32 sum (q-c)^2 of one candidate, packed: ((q0-c0)^2 + (q2-c2)^2) +
@@ -262,9 +426,132 @@ __device__ __forceinline__ void push_redo(const TileArgs& a, bool redo, int32_t 
     if (redo) a.redo[base + __popc(bal & lanemask_lt())] = p;
 }
 
+// Finish query j of the tile (warp-cooperative; lanes over its list entries):
+// float64 keys in the reference's operation order (pyx:32-48, no FMA) ->
+// float32 keys; certificate (>= need entries strictly inside tau_j); counting
+// sort into kBkt buckets on (key/tau)^(d/2) (uniform for uniform density) with
+// __match_any groups; odd-even transposition inside buckets; equal float32
+// keys among the decided entries -> exact path; the sorted row (self first) is
+// written coalesced.  Returns false when the query must be redone.
+template <int DB>
+__device__ __noinline__ bool finish_query(TileWarp& W, const TileArgs& a, int j, int m_l,
+                                          const float4 q, int32_t p, float tau, int32_t qid_l,
+                                          int need) {
+    const float qa[4] = {q.x, q.y, q.z, q.w};
+    const int lane = lane_id();
+    const int m = __shfl_sync(FG_FULL_MASK, m_l, j);
+    const int32_t pj = __shfl_sync(FG_FULL_MASK, p, j);
+    const float tj = __shfl_sync(FG_FULL_MASK, tau, j);
+    double qd[DB];
+#pragma unroll
+    for (int i = 0; i < DB; ++i) qd[i] = (double)__shfl_sync(FG_FULL_MASK, qa[i], j);
+    const float inner = tj * (1.0f - 3e-5f);
+    const float inv_tau = 1.0f / tj;
+    const uint16_t* L = &W.code[j * kStride];
+    constexpr int R = (kCap + 31) / 32;
+    float key[R];
+    uint16_t cd[R];
+    int32_t cpos[R];
+    float4 c[R];
+#pragma unroll
+    for (int t = 0; t < R; ++t) {  // loads first: R gathers in flight
+        const int e = lane + 32 * t;
+        cd[t] = e < m ? L[e] : 0;
+        cpos[t] = W.spS[cd[t] >> 7] + (cd[t] & 127);
+        if (e < m) c[t] = a.sc[cpos[t]];
+    }
+    int n_in = 0;
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+        key[t] = kInf;
+        if (lane + 32 * t < m && cpos[t] != pj) {
+            const float cc[4] = {c[t].x, c[t].y, c[t].z, c[t].w};
+            double acc = 0.0;
+#pragma unroll
+            for (int i = 0; i < DB; ++i) {
+                const double d = __dsub_rn(qd[i], (double)cc[i]);
+                acc = i == 0 ? __dmul_rn(d, d) : __dadd_rn(acc, __dmul_rn(d, d));
+            }
+            key[t] = __double2float_rn(acc);
+            n_in += key[t] < inner ? 1 : 0;
+        }
+    }
+    if (__reduce_add_sync(FG_FULL_MASK, n_in) < need) return false;
+    // counting sort by bucket
+    W.bcnt[lane] = 0u;
+    W.bcnt[lane + 32] = 0u;
+    __syncwarp();
+    int bk[R], idx[R];
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+        bk[t] = key[t] < kInf ? bucket_of<DB>(key[t], inv_tau) : kBkt;
+        const unsigned mm = __match_any_sync(FG_FULL_MASK, bk[t]);
+        const int leader = __ffs(mm) - 1;
+        unsigned old = 0;
+        if (lane == leader && bk[t] < kBkt) old = atomicAdd(&W.bcnt[bk[t]], (unsigned)__popc(mm));
+        idx[t] = (int)__shfl_sync(FG_FULL_MASK, old, leader) + __popc(mm & lanemask_lt());
+    }
+    __syncwarp();
+    const unsigned c0 = W.bcnt[2 * lane], c1 = W.bcnt[2 * lane + 1];
+    const unsigned incl = warp_inclusive_scan(c0 + c1);
+    const int n_valid = (int)__shfl_sync(FG_FULL_MASK, incl, 31);
+    const int maxb = (int)__reduce_max_sync(FG_FULL_MASK, max(c0, c1));
+    __syncwarp();
+    W.bcnt[2 * lane] = incl - c0 - c1;
+    W.bcnt[2 * lane + 1] = incl - c1;
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+        if (bk[t] < kBkt) {
+            const int at = (int)W.bcnt[bk[t]] + idx[t];
+            W.skey[at] = key[t];
+            W.scd[at] = cd[t];
+        }
+    }
+    __syncwarp();
+    // inversions exist only inside buckets (<= maxb entries): maxb odd-even passes
+    for (int pass = 1; pass < maxb; ++pass) {
+#pragma unroll
+        for (int ph = 0; ph < 2; ++ph) {
+#pragma unroll
+            for (int h = 0; h < (kCap + 63) / 64; ++h) {
+                const int i = 2 * (lane + 32 * h) + ph;
+                if (i + 1 < n_valid) {
+                    const float k0 = W.skey[i], k1 = W.skey[i + 1];
+                    if (k0 > k1) {
+                        const uint16_t d0 = W.scd[i], d1 = W.scd[i + 1];
+                        W.skey[i] = k1; W.skey[i + 1] = k0;
+                        W.scd[i] = d1; W.scd[i + 1] = d0;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    }
+    // equal float32 keys among the decided entries: the exact path decides
+    bool amb = false;
+    for (int i = lane; i < need && i + 1 < n_valid; i += 32) amb |= W.skey[i] == W.skey[i + 1];
+    if (__any_sync(FG_FULL_MASK, amb)) return false;
+    const int32_t qid = __shfl_sync(FG_FULL_MASK, qid_l, j);
+    int32_t* oi = a.out_idx + (int64_t)qid * a.k;
+    float* od = a.out_d2 + (int64_t)qid * a.k;
+    for (int sl = lane; sl < a.k; sl += 32) {
+        if (sl == 0) {
+            oi[0] = qid;
+            od[0] = 0.0f;
+        } else {
+            const uint16_t code = W.scd[sl - 1];
+            oi[sl] = a.sid[W.spS[code >> 7] + (code & 127)];
+            od[sl] = W.skey[sl - 1];
+        }
+    }
+    __syncwarp();
+    return true;
+}
+
 // ---------------------------------------------------------------- search
 template <int DB>
-__global__ void __launch_bounds__(kWarps * 32, 2) k_tile_search(const __grid_constant__ TileArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, 4) k_tile_search(const __grid_constant__ TileArgs a) {
     constexpr int NL = DB - 1;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TileWarp& W = reinterpret_cast<TileWarp*>(smem_raw)[threadIdx.x >> 5];
@@ -272,7 +559,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_tile_search(const __grid_con
     const int nb = a.nb;
     const int need = a.k - 1;
     const int n_tiles = a.ctr[0];
-    unsigned long long st_cand = 0, st_tiles = 0, st_redo = 0, st_fail = 0;
+    unsigned long long st_cand = 0, st_tiles = 0, st_redo = 0, st_fail = 0, st_exp = 0;
 
     for (;;) {
         int t = 0;
@@ -457,143 +744,56 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_tile_search(const __grid_con
 
         // ---- scan: 32 candidates per chunk, broadcast to every lane
         const QP qv = pack_q(q);
-        const uint32_t lbase = (uint32_t)__cvta_generic_to_shared(&W.code[lane]);
-        const uint32_t llim = lbase + kCap * 64;
-        const uint32_t sx_addr = (uint32_t)__cvta_generic_to_shared(&W.sx[0][0]);
+        const uint32_t lbase = (uint32_t)__cvta_generic_to_shared(&W.code[lane * kStride]);
+        const uint32_t llim = lbase + kCap * 2;
         uint32_t ptr = lbase;
         bool overflow = false;
-        int s0 = 0;
-        for (int f0 = 0; f0 < T; f0 += 32) {
-            const int f = f0 + lane;
-            const int si = s0 + lane;
-            const int st = si < nsp ? W.spE[si] : 0x7fffffff;
-            const unsigned starts = __reduce_or_sync(
-                FG_FULL_MASK, (lane > 0 && st > f0 && st < f0 + 32) ? 1u << (st - f0) : 0u);
-            const int g = s0 + __popc(starts & ((2u << lane) - 1u));
-            float4 c = make_float4(kInf, kInf, kInf, kInf);
-            uint32_t code = 0;
-            if (f < T) {
-                const int off = f - W.spE[g];
-                c = a.sc[W.spS[g] + off];
-                code = (uint32_t)((g << 7) | off);
-            }
-            W.sx[0][lane] = c.x;
-            W.sx[1][lane] = c.y;
-            W.sx[2][lane] = c.z;
-            W.sx[3][lane] = c.w;
-            W.scode[lane] = code;
-            s0 = __shfl_sync(FG_FULL_MASK, g, 31);
-            if (s0 + 1 < nsp && W.spE[s0 + 1] == f0 + 32) ++s0;
-            __syncwarp();
-            uint32_t cd[32];  // the chunk's codes (uniform), in registers
+        // expanded form around the bbox centre when its error bound allows
+        float cq[4] = {0.f, 0.f, 0.f, 0.f};
+        float rc2 = 0.0f;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const uint4 v = reinterpret_cast<const uint4*>(W.scode)[j];
-                cd[4 * j] = v.x; cd[4 * j + 1] = v.y; cd[4 * j + 2] = v.z; cd[4 * j + 3] = v.w;
-            }
-            // software pipeline: the next group's loads precede this group's stores
-            G4 gb[2];
-            load_g4(gb[0], sx_addr, 0);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                if (j + 1 < 8) load_g4(gb[(j + 1) & 1], sx_addr, 4 * (j + 1));
-                eval_g4(gb[j & 1], qv, tau, ptr, cd[4 * j], cd[4 * j + 1], cd[4 * j + 2],
-                        cd[4 * j + 3]);
-            }
-            if (ptr > llim) {
-                overflow = true;
-                ptr = llim;
-            }
-            __syncwarp();
+        for (int i = 0; i < DB; ++i) {
+            cq[i] = mn[i] + 0.5f * (lo[i] + hi[i]) * w[i];
+            const float rci = rr_max * invw[i] + kSlackCells;
+            const float blo = mn[i] + fmaxf(floorf(lo[i] - rci), 0.0f) * w[i];
+            const float bhi = mn[i] + (fminf(floorf(hi[i] + rci), (float)(nb - 1)) + 1.0f) * w[i];
+            const float e = fmaxf(fabsf(blo - cq[i]), fabsf(bhi - cq[i]));
+            rc2 = fmaf(e, e, rc2);
         }
+        const float4 cen = make_float4(cq[0], cq[1], cq[2], cq[3]);
+        const float4 qs = make_float4(q.x - cen.x, q.y - cen.y, q.z - cen.z, q.w - cen.w);
+        const float sq = fmaf(qs.w, qs.w, fmaf(qs.z, qs.z, fmaf(qs.y, qs.y, qs.x * qs.x)));
+        const float rq = warp_max_f(active ? sqrtf(sq) : 0.0f);
+        const float tau_min = warp_min_f(active ? tau : kInf);
+        const float rsum = (rq + sqrtf(rc2)) * 1.01f;
+        const bool expanded = rsum * rsum <= 32.0f * tau_min;
+        QX qx;
+        qx.sq = pack2(sq);
+        qx.m2q[0] = pack2(-2.0f * qs.x);
+        qx.m2q[1] = pack2(-2.0f * qs.y);
+        qx.m2q[2] = pack2(-2.0f * qs.z);
+        qx.m2q[3] = pack2(-2.0f * qs.w);
+        st_exp += expanded ? 1 : 0;
+        if (expanded)
+            scan_tile<true>(W, a.sc, T, nsp, qv, qx, cen, tau, ptr, overflow, llim);
+        else
+            scan_tile<false>(W, a.sc, T, nsp, qv, qx, cen, tau, ptr, overflow, llim);
         asm volatile("" ::: "memory");  // list stores (inline asm) before the epilogue reads
 
-        // ---- epilogue (per lane)
-        const int m = (int)(ptr - lbase) >> 6;
-        bool ok = active && !overflow;
-        const float inner = tau * (1.0f - 3e-5f);
-        const float inv_tau = tau > 0.0f ? 1.0f / tau : 0.0f;
-        uint8_t* hist = &W.hist[lane * kHistStride];
-#pragma unroll
-        for (int b = 0; b < kBkt; b += 4) *reinterpret_cast<uint32_t*>(hist + b) = 0u;
-        int n_in = 0;
-        const int m_run = ok ? m : 0;
-        for (int e = 0; e < m_run; ++e) {
-            const uint16_t cd = W.code[e * 32 + lane];
-            const int32_t cpos = W.spS[cd >> 7] + (cd & 127);
-            float key = kInf;
-            if (cpos != p) {
-                key = d2_f32(qv, a.sc[cpos]);
-                n_in += key < inner ? 1 : 0;
-                hist[bucket_of<DB>(key, inv_tau)]++;
-            }
-            W.key[e * 32 + lane] = key;
-        }
-        ok &= n_in >= need;
-        // buckets up to the one holding the need-th entry, plus one
-        int M = 0, bstar = kBkt;
-        if (ok) {
-            int cum = 0;
-            for (int b = 0; b < kBkt; ++b) {
-                const int h = hist[b];
-                hist[b] = (uint8_t)cum;
-                cum += h;
-                if (bstar == kBkt && cum >= need) bstar = b;
-                if (b <= bstar + 1) M = cum;
-            }
-            for (int e = 0; e < m; ++e) {
-                const float key = W.key[e * 32 + lane];
-                if (key < kInf) {
-                    const int b = bucket_of<DB>(key, inv_tau);
-                    if (b <= bstar + 1) {
-                        const int sl = hist[b];
-                        hist[b] = (uint8_t)(sl + 1);
-                        W.order[sl * 32 + lane] = (uint8_t)e;
-                    }
-                }
-            }
-            // float64 keys for the decided range, then insertion sort
-            for (int sl = 0; sl < M; ++sl) {
-                const int e = W.order[sl * 32 + lane];
-                const uint16_t cd = W.code[e * 32 + lane];
-                const float4 c = a.sc[W.spS[cd >> 7] + (cd & 127)];
-                const float cq[4] = {c.x, c.y, c.z, c.w};
-                W.key[e * 32 + lane] = __double2float_rn(exact_d2<DB>(qa, cq, DB));
-            }
-            for (int sl = 1; sl < M; ++sl) {
-                const int x = W.order[sl * 32 + lane];
-                const float kx = W.key[x * 32 + lane];
-                int t2 = sl - 1;
-                int y = W.order[t2 * 32 + lane];
-                while (W.key[y * 32 + lane] > kx) {
-                    W.order[(t2 + 1) * 32 + lane] = (uint8_t)y;
-                    if (--t2 < 0) break;
-                    y = W.order[t2 * 32 + lane];
-                }
-                W.order[(t2 + 1) * 32 + lane] = (uint8_t)x;
-            }
-            bool amb = false;
-            float prev = W.key[W.order[lane] * 32 + lane];
-            for (int sl = 1; sl < min(M, need + 1); ++sl) {
-                const float kk = W.key[W.order[sl * 32 + lane] * 32 + lane];
-                amb |= kk == prev;
-                prev = kk;
-            }
-            ok &= !amb;
-        }
-        // ---- output rows (sorted), or the exact path
-        if (ok) {
-            const int32_t qid = a.sid[p];
-            int32_t* oi = a.out_idx + (int64_t)qid * a.k;
-            float* od = a.out_d2 + (int64_t)qid * a.k;
-            oi[0] = qid;
-            od[0] = 0.0f;
-            for (int sl = 0; sl < need; ++sl) {
-                const int e = W.order[sl * 32 + lane];
-                const uint16_t cd = W.code[e * 32 + lane];
-                oi[1 + sl] = a.sid[W.spS[cd >> 7] + (cd & 127)];
-                od[1 + sl] = W.key[e * 32 + lane];
-            }
+        // ---- epilogue: the warp finishes the lanes' queries one at a time
+        const int m_l = (int)(ptr - lbase) >> 1;
+#if defined(FG_TILE_SCAN_ONLY)  // timing experiment: no epilogue (wrong results)
+        if (active && m_l == 1000) a.out_idx[p] = m_l;
+        __syncwarp();
+        continue;
+#endif
+        const unsigned todo = __ballot_sync(FG_FULL_MASK, active && !overflow);
+        bool ok = false;  // this lane's query got its row
+        const int32_t qid_l = active ? a.sid[p] : 0;
+        for (unsigned mask = todo; mask; mask &= mask - 1) {
+            const int j = __ffs(mask) - 1;
+            const bool okj = finish_query<DB>(W, a, j, m_l, q, p, tau, qid_l, need);
+            if (lane == j) ok = okj;
         }
         const bool redo = active && !ok;
         push_redo(a, redo, p);
@@ -607,6 +807,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_tile_search(const __grid_con
             atomicAdd(&a.stats[TS_CAND], st_cand);
             atomicAdd(&a.stats[TS_REDO], st_redo);
             atomicAdd(&a.stats[TS_TILE_FAIL], st_fail);
+            atomicAdd(&a.stats[TS_EXPANDED], st_exp);
         }
     }
 }
