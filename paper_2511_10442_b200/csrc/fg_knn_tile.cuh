@@ -81,8 +81,10 @@ struct TileArgs {
 struct TileWarp {
     uint16_t code[32 * kStride];          // [lane][slot] per-lane candidate lists
     float skey[kCap];                     // epilogue staging of one query: keys
-    uint16_t scd[kCap];                   //   and codes, in (bucket, key) order
-    uint32_t bcnt[kBkt];                  //   bucket counts -> starts
+    int32_t sid[kCap];                    //   and original ids, in bucket order
+    alignas(16) float okey[kCap + 4];     //   final row: slot 0 = self, then by key
+    alignas(16) int32_t oid[kCap + 4];
+    uint32_t bcnt[kBkt + 1];              //   bucket counts -> starts
     int32_t spS[kMaxSpans];               // span start (sorted position)
     uint16_t spE[kMaxSpans + 1];          // span flattened start (exclusive prefix)
     alignas(16) float sx[4][32];          // chunk coordinates, SoA (centred in expanded mode)
@@ -433,13 +435,42 @@ __device__ __forceinline__ void push_redo(const TileArgs& a, bool redo, int32_t 
 // __match_any groups; odd-even transposition inside buckets; equal float32
 // keys among the decided entries -> exact path; the sorted row (self first) is
 // written coalesced.  Returns false when the query must be redone.
+constexpr int kRounds = (kCap + 31) / 32;
+
+// Global gathers of one query's list (coordinates and original ids of its
+// entries): issued for query j+1 while query j is being finished.
+struct QLoads {
+    float4 c[kRounds];
+    int32_t cpos[kRounds];
+    int32_t id[kRounds];
+    int m;
+};
+
+__device__ __forceinline__ void fetch_query(const TileWarp& W, const TileArgs& a, int j, int m_l,
+                                            QLoads& Q) {
+    const int lane = lane_id();
+    Q.m = __shfl_sync(FG_FULL_MASK, m_l, j);
+    const uint16_t* L = &W.code[j * kStride];
+#pragma unroll
+    for (int t = 0; t < kRounds; ++t) {
+        const int e = lane + 32 * t;
+        Q.cpos[t] = -1;
+        if (32 * t < Q.m && e < Q.m) {  // 32t < m is warp-uniform
+            const uint16_t cd = L[e];
+            Q.cpos[t] = W.spS[cd >> 7] + (cd & 127);
+            Q.c[t] = a.sc[Q.cpos[t]];
+            Q.id[t] = a.sid[Q.cpos[t]];
+        }
+    }
+}
+
 template <int DB>
-__device__ __noinline__ bool finish_query(TileWarp& W, const TileArgs& a, int j, int m_l,
-                                          const float4 q, int32_t p, float tau, int32_t qid_l,
-                                          int need) {
+__device__ __forceinline__ bool finish_query(TileWarp& W, const TileArgs& a, int j, const QLoads& Q,
+                                             const float4 q, int32_t p, float tau, int32_t qid_l,
+                                             int need) {
     const float qa[4] = {q.x, q.y, q.z, q.w};
     const int lane = lane_id();
-    const int m = __shfl_sync(FG_FULL_MASK, m_l, j);
+    const int m = Q.m;
     const int32_t pj = __shfl_sync(FG_FULL_MASK, p, j);
     const float tj = __shfl_sync(FG_FULL_MASK, tau, j);
     double qd[DB];
@@ -447,24 +478,16 @@ __device__ __noinline__ bool finish_query(TileWarp& W, const TileArgs& a, int j,
     for (int i = 0; i < DB; ++i) qd[i] = (double)__shfl_sync(FG_FULL_MASK, qa[i], j);
     const float inner = tj * (1.0f - 3e-5f);
     const float inv_tau = 1.0f / tj;
-    const uint16_t* L = &W.code[j * kStride];
-    constexpr int R = (kCap + 31) / 32;
+    constexpr int R = kRounds;
     float key[R];
-    uint16_t cd[R];
-    int32_t cpos[R];
-    float4 c[R];
 #pragma unroll
-    for (int t = 0; t < R; ++t) {  // loads first: R gathers in flight
-        const int e = lane + 32 * t;
-        cd[t] = e < m ? L[e] : 0;
-        cpos[t] = W.spS[cd[t] >> 7] + (cd[t] & 127);
-        if (e < m) c[t] = a.sc[cpos[t]];
-    }
+    for (int t = 0; t < R; ++t) key[t] = kInf;
+    const int32_t* cpos = Q.cpos;
+    const float4* c = Q.c;
     int n_in = 0;
 #pragma unroll
     for (int t = 0; t < R; ++t) {
-        key[t] = kInf;
-        if (lane + 32 * t < m && cpos[t] != pj) {
+        if (cpos[t] >= 0 && cpos[t] != pj) {
             const float cc[4] = {c[t].x, c[t].y, c[t].z, c[t].w};
             double acc = 0.0;
 #pragma unroll
@@ -477,7 +500,7 @@ __device__ __noinline__ bool finish_query(TileWarp& W, const TileArgs& a, int j,
         }
     }
     if (__reduce_add_sync(FG_FULL_MASK, n_in) < need) return false;
-    // counting sort by bucket
+    // counting sort by bucket: counts (match_any groups + one smem atomic per group)
     W.bcnt[lane] = 0u;
     W.bcnt[lane + 32] = 0u;
     __syncwarp();
@@ -485,64 +508,81 @@ __device__ __noinline__ bool finish_query(TileWarp& W, const TileArgs& a, int j,
 #pragma unroll
     for (int t = 0; t < R; ++t) {
         bk[t] = key[t] < kInf ? bucket_of<DB>(key[t], inv_tau) : kBkt;
-        const unsigned mm = __match_any_sync(FG_FULL_MASK, bk[t]);
-        const int leader = __ffs(mm) - 1;
-        unsigned old = 0;
-        if (lane == leader && bk[t] < kBkt) old = atomicAdd(&W.bcnt[bk[t]], (unsigned)__popc(mm));
-        idx[t] = (int)__shfl_sync(FG_FULL_MASK, old, leader) + __popc(mm & lanemask_lt());
+        idx[t] = 0;
+        if (32 * t < m) {
+            const unsigned mm = __match_any_sync(FG_FULL_MASK, bk[t]);
+            const int leader = __ffs(mm) - 1;
+            unsigned old = 0;
+            if (lane == leader && bk[t] < kBkt)
+                old = atomicAdd(&W.bcnt[bk[t]], (unsigned)__popc(mm));
+            idx[t] = (int)__shfl_sync(FG_FULL_MASK, old, leader) + __popc(mm & lanemask_lt());
+        }
     }
     __syncwarp();
     const unsigned c0 = W.bcnt[2 * lane], c1 = W.bcnt[2 * lane + 1];
     const unsigned incl = warp_inclusive_scan(c0 + c1);
     const int n_valid = (int)__shfl_sync(FG_FULL_MASK, incl, 31);
-    const int maxb = (int)__reduce_max_sync(FG_FULL_MASK, max(c0, c1));
     __syncwarp();
     W.bcnt[2 * lane] = incl - c0 - c1;
     W.bcnt[2 * lane + 1] = incl - c1;
+    if (lane == 31) W.bcnt[kBkt] = incl;
     __syncwarp();
 #pragma unroll
     for (int t = 0; t < R; ++t) {
         if (bk[t] < kBkt) {
             const int at = (int)W.bcnt[bk[t]] + idx[t];
             W.skey[at] = key[t];
-            W.scd[at] = cd[t];
+            W.sid[at] = Q.id[t];
         }
     }
     __syncwarp();
-    // inversions exist only inside buckets (<= maxb entries): maxb odd-even passes
-    for (int pass = 1; pass < maxb; ++pass) {
+    // final slot = bucket start + rank inside the bucket (a uniform maxb-step
+    // loop); only buckets starting at or below `need` can reach the decided
+    // range.  Equal float32 keys there: the exact path decides.
+    bool amb = false;
 #pragma unroll
-        for (int ph = 0; ph < 2; ++ph) {
-#pragma unroll
-            for (int h = 0; h < (kCap + 63) / 64; ++h) {
-                const int i = 2 * (lane + 32 * h) + ph;
-                if (i + 1 < n_valid) {
-                    const float k0 = W.skey[i], k1 = W.skey[i + 1];
-                    if (k0 > k1) {
-                        const uint16_t d0 = W.scd[i], d1 = W.scd[i + 1];
-                        W.skey[i] = k1; W.skey[i + 1] = k0;
-                        W.scd[i] = d1; W.scd[i + 1] = d0;
-                    }
+    for (int t = 0; t < R; ++t) {
+        const int sl = lane + 32 * t;
+        if (32 * t < n_valid) {
+            const bool valid = sl < n_valid;
+            const float kk = W.skey[valid ? sl : 0];
+            const int b = bucket_of<DB>(kk, inv_tau);
+            const int b0 = (int)W.bcnt[b], b1 = (int)W.bcnt[b + 1];
+            const bool live = valid && b0 <= need;
+            int r = b0;
+            bool tie = false;
+            if (live) {
+                for (int i = b0; i < b1; ++i) {
+                    const float ki = W.skey[i];
+                    r += (ki < kk || (ki == kk && i < sl)) ? 1 : 0;
+                    tie |= ki == kk && i != sl;
                 }
             }
-            __syncwarp();
+            if (live) {
+                W.okey[r + 1] = kk;
+                W.oid[r + 1] = W.sid[sl];
+            }
+            amb |= tie && r < need;
         }
     }
-    // equal float32 keys among the decided entries: the exact path decides
-    bool amb = false;
-    for (int i = lane; i < need && i + 1 < n_valid; i += 32) amb |= W.skey[i] == W.skey[i + 1];
     if (__any_sync(FG_FULL_MASK, amb)) return false;
     const int32_t qid = __shfl_sync(FG_FULL_MASK, qid_l, j);
+    if (lane == 0) {
+        W.okey[0] = 0.0f;
+        W.oid[0] = qid;
+    }
+    __syncwarp();
     int32_t* oi = a.out_idx + (int64_t)qid * a.k;
     float* od = a.out_d2 + (int64_t)qid * a.k;
-    for (int sl = lane; sl < a.k; sl += 32) {
-        if (sl == 0) {
-            oi[0] = qid;
-            od[0] = 0.0f;
-        } else {
-            const uint16_t code = W.scd[sl - 1];
-            oi[sl] = a.sid[W.spS[code >> 7] + (code & 127)];
-            od[sl] = W.skey[sl - 1];
+    if ((a.k & 3) == 0) {  // 16-byte row segments
+        for (int g = lane; 4 * g < a.k; g += 32) {
+            *reinterpret_cast<int4*>(oi + 4 * g) = *reinterpret_cast<const int4*>(&W.oid[4 * g]);
+            *reinterpret_cast<float4*>(od + 4 * g) = *reinterpret_cast<const float4*>(&W.okey[4 * g]);
+        }
+    } else {
+        for (int sl = lane; sl < a.k; sl += 32) {
+            oi[sl] = W.oid[sl];
+            od[sl] = W.okey[sl];
         }
     }
     __syncwarp();
@@ -790,10 +830,15 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_tile_search(const __grid_con
         const unsigned todo = __ballot_sync(FG_FULL_MASK, active && !overflow);
         bool ok = false;  // this lane's query got its row
         const int32_t qid_l = active ? a.sid[p] : 0;
-        for (unsigned mask = todo; mask; mask &= mask - 1) {
+        QLoads cur, nxt;
+        if (todo) fetch_query(W, a, __ffs(todo) - 1, m_l, cur);
+        for (unsigned mask = todo; mask;) {
             const int j = __ffs(mask) - 1;
-            const bool okj = finish_query<DB>(W, a, j, m_l, q, p, tau, qid_l, need);
+            mask &= mask - 1;
+            if (mask) fetch_query(W, a, __ffs(mask) - 1, m_l, nxt);  // next query's gathers
+            const bool okj = finish_query<DB>(W, a, j, cur, q, p, tau, qid_l, need);
             if (lane == j) ok = okj;
+            cur = nxt;
         }
         const bool redo = active && !ok;
         push_redo(a, redo, p);
