@@ -94,6 +94,102 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_knn_bwd(const float* __restr
     }
 }
 
+// d <= 4, k <= 65: RPW rows per warp with every (row, slot-round) chain in
+// flight at once -- the coordinate gathers, then the returning fp32x4 atomics,
+// then the TwoSum corrections -- so the L2 round trips of 2*RPW chains overlap
+// (the warp-per-row kernel above waits for each one).  Same arithmetic.
+template <int RPW, int SR>
+__global__ void __launch_bounds__(kRowWarps * 32) k_knn_bwd_pipe(
+    const float* __restrict__ coords, int64_t n, int n_c, const int32_t* __restrict__ idx, int k,
+    const float* __restrict__ gd2, const int32_t* __restrict__ order, float4* __restrict__ hi,
+    float4* __restrict__ lo) {
+    constexpr int C = RPW * SR;
+    const int lane = lane_id();
+    const int64_t p0 = (blockIdx.x * (int64_t)kRowWarps + (threadIdx.x >> 5)) * RPW;
+    if (p0 >= n) return;
+    int64_t v[RPW];
+    int32_t u[C];
+    float g[C];
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+        const int64_t pr = min(p0 + r, n - 1);
+        v[r] = order ? (int64_t)order[pr] : pr;
+    }
+#pragma unroll
+    for (int r = 0; r < RPW; ++r)
+#pragma unroll
+        for (int q = 0; q < SR; ++q) {
+            const int s = 1 + lane + 32 * q;
+            const bool ok = p0 + r < n && s < k;
+            u[r * SR + q] = ok ? idx[v[r] * k + s] : -1;
+            g[r * SR + q] = ok ? gd2[v[r] * k + s] : 0.0f;
+        }
+    auto load4 = [&](int64_t w) {
+        if (n_c == 4) return reinterpret_cast<const float4*>(coords)[w];
+        float t[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int i = 0; i < n_c; ++i) t[i] = coords[w * n_c + i];
+        return make_float4(t[0], t[1], t[2], t[3]);
+    };
+    float4 xv[RPW], xu[C];
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) xv[r] = load4(v[r]);
+#pragma unroll
+    for (int c = 0; c < C; ++c) xu[c] = u[c] >= 0 ? load4(u[c]) : xv[c / SR];
+    // returning hi atomics for every chain, then the corrections
+    float4 h[C], old[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        const double tg = 2.0 * (double)g[c];
+        const float4 a = xv[c / SR], b = xu[c];
+        h[c] = make_float4((float)-(tg * ((double)a.x - (double)b.x)), (float)-(tg * ((double)a.y - (double)b.y)),
+                           (float)-(tg * ((double)a.z - (double)b.z)), (float)-(tg * ((double)a.w - (double)b.w)));
+        if (u[c] >= 0) old[c] = atomicAdd(hi + u[c], h[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        if (u[c] < 0) continue;
+        const double tg = 2.0 * (double)g[c];
+        const float4 a = xv[c / SR], b = xu[c];
+        const double x[4] = {-(tg * ((double)a.x - (double)b.x)), -(tg * ((double)a.y - (double)b.y)),
+                             -(tg * ((double)a.z - (double)b.z)), -(tg * ((double)a.w - (double)b.w))};
+        const float* hp = &h[c].x;
+        const float* op = &old[c].x;
+        float4 l;
+        float* lp = &l.x;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            lp[i] = (float)(x[i] - (double)hp[i]);
+            const float a2 = op[i], b2 = hp[i];
+            const float sum = __fadd_rn(a2, b2);
+            const float bb = __fsub_rn(sum, a2);
+            const float err = __fadd_rn(__fsub_rn(a2, __fsub_rn(sum, bb)), __fsub_rn(b2, bb));
+            lp[i] = __fadd_rn(lp[i], err);
+        }
+        atomicAdd(lo + u[c], l);
+    }
+    // query side: per row, the sum of its terms (float64 warp reduction)
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+        double qs[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int q = 0; q < SR; ++q) {
+            const int c = r * SR + q;
+            if (u[c] < 0) continue;
+            const double tg = 2.0 * (double)g[c];
+            const float4 a = xv[r], b = xu[c];
+            qs[0] += tg * ((double)a.x - (double)b.x);
+            qs[1] += tg * ((double)a.y - (double)b.y);
+            qs[2] += tg * ((double)a.z - (double)b.z);
+            qs[3] += tg * ((double)a.w - (double)b.w);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) qs[i] += __shfl_xor_sync(FG_FULL_MASK, qs[i], o);
+        if (lane == 0 && p0 + r < n) two_sum_add(hi + v[r], lo + v[r], qs);
+    }
+}
+
 __global__ void k_bwd_finish(const float4* __restrict__ hi, const float4* __restrict__ lo, int64_t n,
                              int n_c, int nv, void* __restrict__ out, int is_f64) {
     const int64_t m = n * n_c;
@@ -142,7 +238,16 @@ extern "C" int fg_knn_bwd(const float* coords, int64_t n, int32_t n_coords, cons
     float4* lo = (float4*)((char*)workspace + half);
     FG_CUDA(cudaMemsetAsync(workspace, 0, 2 * half, st));
     const unsigned blocks = (unsigned)ceil_div(n, kRowWarps);
-    switch (nv) {
+#ifndef FG_BWD_RPW
+#define FG_BWD_RPW 2
+#endif
+    constexpr int RPW = FG_BWD_RPW;
+    const unsigned pblocks = (unsigned)ceil_div(n, (int64_t)kRowWarps * RPW);
+    if (nv == 1 && k <= 33) {
+        k_knn_bwd_pipe<RPW, 1><<<pblocks, kRowWarps * 32, 0, st>>>(coords, n, n_coords, idx, k, grad_d2, order, hi, lo);
+    } else if (nv == 1 && k <= 65) {
+        k_knn_bwd_pipe<RPW, 2><<<pblocks, kRowWarps * 32, 0, st>>>(coords, n, n_coords, idx, k, grad_d2, order, hi, lo);
+    } else switch (nv) {
         case 1: k_knn_bwd<1><<<blocks, kRowWarps * 32, 0, st>>>(coords, n, n_coords, idx, k, grad_d2, order, hi, lo); break;
         case 2: k_knn_bwd<2><<<blocks, kRowWarps * 32, 0, st>>>(coords, n, n_coords, idx, k, grad_d2, order, hi, lo); break;
         case 3: k_knn_bwd<3><<<blocks, kRowWarps * 32, 0, st>>>(coords, n, n_coords, idx, k, grad_d2, order, hi, lo); break;
