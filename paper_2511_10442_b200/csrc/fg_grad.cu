@@ -239,7 +239,7 @@ extern "C" int fg_knn_bwd(const float* coords, int64_t n, int32_t n_coords, cons
     FG_CUDA(cudaMemsetAsync(workspace, 0, 2 * half, st));
     const unsigned blocks = (unsigned)ceil_div(n, kRowWarps);
 #ifndef FG_BWD_RPW
-#define FG_BWD_RPW 2
+#define FG_BWD_RPW 1
 #endif
     constexpr int RPW = FG_BWD_RPW;
     const unsigned pblocks = (unsigned)ceil_div(n, (int64_t)kRowWarps * RPW);

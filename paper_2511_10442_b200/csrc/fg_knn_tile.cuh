@@ -135,19 +135,27 @@ __global__ void __launch_bounds__(128) k_tiles(const TileArgs a) {
         }
     }
     const int P = warp_inclusive_scan(col);
-    int start = 0, base = 0;
-    while (start < nb) {  // warp-uniform greedy segmentation
+    // warp-uniform greedy segmentation (P is non-decreasing: each segment is a
+    // prefix run of the remaining columns), tiles staged in registers and
+    // claimed with one atomic per block
+    int start = 0, base = 0, nt = 0;
+    int2 mine = make_int2(0, 0);
+    while (start < nb) {
         const unsigned bal = __ballot_sync(FG_FULL_MASK, lane >= start && lane < nb && P - base <= 32);
-        const int end = bal ? 31 - __clz(bal) : start;  // P is non-decreasing: a prefix run
+        const int end = bal ? 31 - __clz(bal) : start;
         const int pe = __shfl_sync(FG_FULL_MASK, P, end);
         const int cnt = pe - base;
-        if (cnt > 0 && lane == 0) {
-            const int t = atomicAdd(&a.ctr[0], 1);
-            a.tiles[t] = make_int2(blk, start | (end << 8) | (min(cnt, 32767) << 16));
+        if (cnt > 0) {
+            if (lane == nt) mine = make_int2(blk, start | (end << 8) | (min(cnt, 32767) << 16));
+            ++nt;
         }
         base = pe;
         start = end + 1;
     }
+    int t0 = 0;
+    if (lane == 0 && nt > 0) t0 = atomicAdd(&a.ctr[0], nt);
+    t0 = __shfl_sync(FG_FULL_MASK, t0, 0);
+    if (lane < nt) a.tiles[t0 + lane] = mine;
 }
 
 // ---------------------------------------------------------------- helpers
