@@ -336,6 +336,133 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_gn_rows(const GnArgs g, cons
     }
 }
 
+// Single-gather row pass for k <= 64 (2 slot windows): the mean-block dot
+// products and the running arg-max (value, slot, feature value at the max)
+// come out of ONE gather sweep; the max blocks' share of grad_d2 (a few
+// slots per row) is added through shared-memory float64 atomics afterwards,
+// and their feature gradient goes to the arg-max neighbour as before.  Same
+// arithmetic as k_gn_rows (which gathers twice: arg-max first, then the dots).
+template <int VW>
+__global__ void __launch_bounds__(kRowWarps * 32) k_gn_rows1(const GnArgs g, const GnBwd bw, int f0,
+                                                           int last_chunk) {
+    static_assert(U == 8, "transpose_reduce8");
+    __shared__ double extra_s[kRowWarps][64];
+    const int lane = lane_id();
+    const int wi = threadIdx.x >> 5;
+    const int64_t p = blockIdx.x * (int64_t)kRowWarps + wi;
+    if (p >= g.n) return;
+    const int64_t v = row_of(g, p);
+    const int k = g.k, F = g.F, W = F * g.n_red;
+    const int fl = f0 + lane * VW;
+    const bool lane_on = fl < F;
+    const bool has_max = g.max_bits != 0;
+    Window wd[2];
+    int cnt = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        wd[h] = load_window(g, v, 32 * h, true);
+        cnt += __popc(wd[h].okm);
+        if (f0 == 0 && ((wd[h].okm >> lane) & 1u)) atomicAdd(&bw.rev_cnt[wd[h].u], 1);
+    }
+    extra_s[wi][lane] = 0.0;
+    extra_s[wi][lane + 32] = 0.0;
+    double cmean[VW], cmax[VW];
+#pragma unroll
+    for (int e = 0; e < VW; ++e) {
+        cmean[e] = 0.0;
+        cmax[e] = 0.0;
+    }
+    if (lane_on && cnt > 0) {
+        for (int b = 0; b < g.n_red; ++b) {
+            float ub[VW];
+            ldf<VW>(bw.up + v * W + (int64_t)b * F + fl, ub);
+#pragma unroll
+            for (int e = 0; e < VW; ++e) {
+                if (is_max(g, b))
+                    cmax[e] += (double)ub[e];
+                else
+                    cmean[e] += (double)ub[e] / (double)cnt;
+            }
+        }
+    }
+    if (lane_on && bw.has_mean) {
+        float o[VW];
+#pragma unroll
+        for (int e = 0; e < VW; ++e) o[e] = (float)cmean[e];
+        stf<VW>(bw.cm + v * F + fl, o);
+    }
+    double best[VW], bwt[VW];
+    float bx[VW];
+    int bslot[VW];
+#pragma unroll
+    for (int e = 0; e < VW; ++e) {
+        best[e] = -INFINITY;
+        bslot[e] = -1;
+        bwt[e] = 0.0;
+        bx[e] = 0.0f;
+    }
+    double mine[2] = {0.0, 0.0};  // this lane's slot: mean-block dot product
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const unsigned okm = cnt > 0 ? wd[h].okm : 0u;
+        for (int j0 = 0; j0 < 32; j0 += U) {
+            if (((okm >> j0) & ((1u << U) - 1u)) == 0) continue;
+            float x[U][VW];
+            double w[U];
+            bool valid[U];
+            gather<VW>(g, wd[h], j0, fl, lane_on, x, w, valid);
+            double part[U];
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                part[q] = 0.0;
+#pragma unroll
+                for (int e = 0; e < VW; ++e) {
+                    part[q] += (double)x[q][e] * cmean[e];
+                    if (has_max && valid[q]) {
+                        const double term = w[q] * (double)x[q][e];
+                        if (term > best[e]) {
+                            best[e] = term;
+                            bslot[e] = 32 * h + j0 + q;
+                            bwt[e] = w[q];
+                            bx[e] = x[q][e];
+                        }
+                    }
+                }
+            }
+            const double r = transpose_reduce8(part);
+            const double got = __shfl_sync(FG_FULL_MASK, r, reduce8_src((lane - j0) & 7));
+            if (lane >= j0 && lane < j0 + U) mine[h] = got;
+        }
+    }
+    __syncwarp();
+    // max blocks: slot bslot gets -scale w x cmax in grad_d2, neighbour u gets w cmax
+    if (has_max && lane_on && cnt > 0) {
+#pragma unroll
+        for (int e = 0; e < VW; ++e) {
+            if (bslot[e] < 0) continue;
+            atomicAdd(&extra_s[wi][bslot[e]], (double)bx[e] * cmax[e]);
+            if (bw.gmax) {
+                const int32_t u = __ldg(&g.idx[v * k + bslot[e]]);
+                atomicAdd(&bw.gmax[(int64_t)u * F + fl + e], bwt[e] * cmax[e]);
+            }
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int s = 32 * h + lane;
+        if (s < k) {
+            const bool ok = cnt > 0 && ((wd[h].okm >> lane) & 1u);
+            double val = ok ? -g.scale * wd[h].w * (mine[h] + extra_s[wi][s]) : 0.0;
+            if (bw.gd_acc) {
+                if (f0 > 0) val += bw.gd_acc[v * k + s];
+                if (!last_chunk) bw.gd_acc[v * k + s] = val;
+            }
+            if (last_chunk) bw.grad_d2[v * k + s] = (float)val;
+        }
+    }
+}
+
 // Reverse fill: entry v*k + s goes to neighbour u's list.
 __global__ void k_gn_fill(const GnArgs g, const GnBwd bw) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -479,7 +606,10 @@ int gn_backward(const GnArgs& g, GnBwd bw, const BwdWs& w, cudaStream_t st) {
     if (g.F <= CW) bw.gd_acc = nullptr;
     const unsigned blocks = (unsigned)ceil_div(g.n, kRowWarps);
     for (int f0 = 0; f0 < g.F; f0 += CW) {
-        k_gn_rows<VW><<<blocks, kRowWarps * 32, 0, st>>>(g, bw, f0, f0 + CW >= g.F);
+        if (g.k <= 64)
+            k_gn_rows1<VW><<<blocks, kRowWarps * 32, 0, st>>>(g, bw, f0, f0 + CW >= g.F);
+        else
+            k_gn_rows<VW><<<blocks, kRowWarps * 32, 0, st>>>(g, bw, f0, f0 + CW >= g.F);
         FG_TRY(launched(st));
     }
     if (bw.has_mean) {
