@@ -49,7 +49,7 @@ constexpr int kWarps = 4;          // warps per CTA (4 CTAs per SM: 16 warps)
 constexpr int kCap = 88;           // list entries per lane
 constexpr int kSlack = 32;         // one chunk of overrun before the clamp
 constexpr int kStride = kCap + kSlack + 2;  // u16 per lane list: 61 words, odd -> bank spread
-constexpr int kBkt = 64;           // epilogue buckets (2 per lane)
+constexpr int kBkt = 256;          // epilogue buckets (8 per lane)
 constexpr int kMaxSpans = 320;     // candidate spans per tile
 constexpr int kMaxSpanLen = 127;   // 7-bit offsets in the codes
 constexpr float kAlpha = 1.12f;    // radius inflation over the density estimate
@@ -84,7 +84,7 @@ struct TileWarp {
     int32_t sid[kCap];                    //   and original ids, in bucket order
     alignas(16) float okey[kCap + 4];     //   final row: slot 0 = self, then by key
     alignas(16) int32_t oid[kCap + 4];
-    uint32_t bcnt[kBkt + 1];              //   bucket counts -> starts
+    alignas(16) uint32_t bcnt[kBkt + 4];  //   bucket counts -> starts
     int32_t spS[kMaxSpans];               // span start (sorted position)
     uint16_t spE[kMaxSpans + 1];          // span flattened start (exclusive prefix)
     alignas(16) float sx[4][32];          // chunk coordinates, SoA (centred in expanded mode)
@@ -509,8 +509,8 @@ __device__ __forceinline__ bool finish_query(TileWarp& W, const TileArgs& a, int
     }
     if (__reduce_add_sync(FG_FULL_MASK, n_in) < need) return false;
     // counting sort by bucket: counts (match_any groups + one smem atomic per group)
-    W.bcnt[lane] = 0u;
-    W.bcnt[lane + 32] = 0u;
+    *reinterpret_cast<uint4*>(&W.bcnt[8 * lane]) = make_uint4(0u, 0u, 0u, 0u);
+    *reinterpret_cast<uint4*>(&W.bcnt[8 * lane + 4]) = make_uint4(0u, 0u, 0u, 0u);
     __syncwarp();
     int bk[R], idx[R];
 #pragma unroll
@@ -527,12 +527,25 @@ __device__ __forceinline__ bool finish_query(TileWarp& W, const TileArgs& a, int
         }
     }
     __syncwarp();
-    const unsigned c0 = W.bcnt[2 * lane], c1 = W.bcnt[2 * lane + 1];
-    const unsigned incl = warp_inclusive_scan(c0 + c1);
+    uint4 ca = *reinterpret_cast<const uint4*>(&W.bcnt[8 * lane]);
+    uint4 cb = *reinterpret_cast<const uint4*>(&W.bcnt[8 * lane + 4]);
+    const unsigned tot = ca.x + ca.y + ca.z + ca.w + cb.x + cb.y + cb.z + cb.w;
+    const unsigned incl = warp_inclusive_scan(tot);
     const int n_valid = (int)__shfl_sync(FG_FULL_MASK, incl, 31);
     __syncwarp();
-    W.bcnt[2 * lane] = incl - c0 - c1;
-    W.bcnt[2 * lane + 1] = incl - c1;
+    {  // exclusive starts of this lane's 8 buckets
+        unsigned run = incl - tot, t0;
+        t0 = ca.x; ca.x = run; run += t0;
+        t0 = ca.y; ca.y = run; run += t0;
+        t0 = ca.z; ca.z = run; run += t0;
+        t0 = ca.w; ca.w = run; run += t0;
+        t0 = cb.x; cb.x = run; run += t0;
+        t0 = cb.y; cb.y = run; run += t0;
+        t0 = cb.z; cb.z = run; run += t0;
+        cb.w = run;
+    }
+    *reinterpret_cast<uint4*>(&W.bcnt[8 * lane]) = ca;
+    *reinterpret_cast<uint4*>(&W.bcnt[8 * lane + 4]) = cb;
     if (lane == 31) W.bcnt[kBkt] = incl;
     __syncwarp();
 #pragma unroll
