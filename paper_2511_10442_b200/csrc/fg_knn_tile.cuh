@@ -368,14 +368,14 @@ __device__ __forceinline__ void scan_tile(TileWarp& W, const float4* __restrict_
         if (EXP) W.sn[lane] = nn;
         W.scode[lane] = code;
         __syncwarp();
-        uint32_t cd[32];  // the chunk's codes (uniform), in registers
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const uint4 v = reinterpret_cast<const uint4*>(W.scode)[j];
-            cd[4 * j] = v.x; cd[4 * j + 1] = v.y; cd[4 * j + 2] = v.z; cd[4 * j + 3] = v.w;
-        }
         // software pipeline: the next group's loads precede this group's stores
         if (EXP) {
+            uint32_t cd[32];  // the chunk's codes (uniform), in registers
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint4 v = reinterpret_cast<const uint4*>(W.scode)[j];
+                cd[4 * j] = v.x; cd[4 * j + 1] = v.y; cd[4 * j + 2] = v.z; cd[4 * j + 3] = v.w;
+            }
             G4X gb[2];
             load_g4x(gb[0], sx_addr, 0);
 #pragma unroll
@@ -385,13 +385,13 @@ __device__ __forceinline__ void scan_tile(TileWarp& W, const float4* __restrict_
                          cd[4 * j + 3]);
             }
         } else {
-            G4 gb[2];
-            load_g4(gb[0], sx_addr, 0);
-#pragma unroll
+            // direct form (the ~10% of tiles the expanded bound rejects): rolled, small code
+#pragma unroll 1
             for (int j = 0; j < 8; ++j) {
-                if (j + 1 < 8) load_g4(gb[(j + 1) & 1], sx_addr, 4 * (j + 1));
-                eval_g4(gb[j & 1], qv, tau, ptr, cd[4 * j], cd[4 * j + 1], cd[4 * j + 2],
-                        cd[4 * j + 3]);
+                G4 gq;
+                load_g4(gq, sx_addr, 4 * j);
+                const uint4 cv = reinterpret_cast<const uint4*>(W.scode)[j];
+                eval_g4(gq, qv, tau, ptr, cv.x, cv.y, cv.z, cv.w);
             }
         }
         if (ptr > llim) {
