@@ -105,12 +105,12 @@ __device__ __forceinline__ Window load_window(const GnArgs& g, int64_t v, int ba
     return wd;
 }
 
-// Gather U slots' feature vectors (warp-uniform validity).
-template <int VW>
+// Gather UU slots' feature vectors (warp-uniform validity).
+template <int VW, int UU = U>
 __device__ __forceinline__ void gather(const GnArgs& g, const Window& wd, int j0, int fl, bool lane_on,
-                                       float (&x)[U][VW], double (&w)[U], bool (&valid)[U]) {
+                                       float (&x)[UU][VW], double (&w)[UU], bool (&valid)[UU]) {
 #pragma unroll
-    for (int q = 0; q < U; ++q) {
+    for (int q = 0; q < UU; ++q) {
         const int jj = j0 + q;
         valid[q] = jj < 32 && ((wd.okm >> (jj & 31)) & 1u);
         const int32_t uq = __shfl_sync(FG_FULL_MASK, wd.u, jj & 31);
@@ -122,8 +122,12 @@ __device__ __forceinline__ void gather(const GnArgs& g, const Window& wd, int j0
 }
 
 // ---------------------------------------------------------------- forward
+#ifndef FG_GN_FWD_U
+#define FG_GN_FWD_U 4
+#endif
 template <int VW>
 __global__ void __launch_bounds__(kRowWarps * 32) k_gn_fwd(const GnArgs g, int f0, float* __restrict__ out) {
+    constexpr int UF = FG_GN_FWD_U;  // gathers in flight per warp
     const int lane = lane_id();
     const int64_t p = blockIdx.x * (int64_t)kRowWarps + (threadIdx.x >> 5);
     if (p >= g.n) return;
@@ -141,14 +145,14 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_gn_fwd(const GnArgs g, int f
     for (int base = 0; base < k; base += 32) {
         const Window wd = load_window(g, v, base, true);
         cnt += __popc(wd.okm);
-        for (int j0 = 0; j0 < 32; j0 += U) {
-            if (((wd.okm >> j0) & ((1u << U) - 1u)) == 0) continue;
-            float x[U][VW];
-            double w[U];
-            bool valid[U];
-            gather<VW>(g, wd, j0, fl, lane_on, x, w, valid);
+        for (int j0 = 0; j0 < 32; j0 += UF) {
+            if (((wd.okm >> j0) & (UF == 32 ? 0xffffffffu : ((1u << UF) - 1u))) == 0) continue;
+            float x[UF][VW];
+            double w[UF];
+            bool valid[UF];
+            gather<VW, UF>(g, wd, j0, fl, lane_on, x, w, valid);
 #pragma unroll
-            for (int q = 0; q < U; ++q) {
+            for (int q = 0; q < UF; ++q) {
                 if (!valid[q]) continue;
 #pragma unroll
                 for (int e = 0; e < VW; ++e) {
@@ -218,6 +222,34 @@ __device__ __forceinline__ double transpose_reduce8(double (&a)[8]) {
 }
 
 __device__ __forceinline__ int reduce8_src(int q) { return ((q >> 2) & 1) << 4 | ((q >> 1) & 1) << 3 | (q & 1) << 2; }
+
+// Sum a[q] over the warp for q = 0..3 at once; lane L ends with the total of
+// q = 2 b4 + b3 (bits of L).
+__device__ __forceinline__ double transpose_reduce4(double (&a)[4]) {
+    const int lane = lane_id();
+    {
+        const bool hi = lane & 16;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const double send = hi ? a[i] : a[i + 2];
+            const double keep = hi ? a[i + 2] : a[i];
+            a[i] = keep + __shfl_xor_sync(FG_FULL_MASK, send, 16);
+        }
+    }
+    {
+        const bool hi = lane & 8;
+        const double send = hi ? a[0] : a[1];
+        const double keep = hi ? a[1] : a[0];
+        a[0] = keep + __shfl_xor_sync(FG_FULL_MASK, send, 8);
+    }
+    double r = a[0];
+    r += __shfl_xor_sync(FG_FULL_MASK, r, 4);
+    r += __shfl_xor_sync(FG_FULL_MASK, r, 2);
+    r += __shfl_xor_sync(FG_FULL_MASK, r, 1);
+    return r;
+}
+
+__device__ __forceinline__ int reduce4_src(int q) { return ((q >> 1) & 1) << 4 | (q & 1) << 3; }
 
 // Row pass: arg-max slots (registers), grad_d2, the mean coefficients cm and
 // the max-block gradients (float64 atomics, one per (v, f) to its arg-max
@@ -345,7 +377,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_gn_rows(const GnArgs g, cons
 template <int VW>
 __global__ void __launch_bounds__(kRowWarps * 32) k_gn_rows1(const GnArgs g, const GnBwd bw, int f0,
                                                            int last_chunk) {
-    static_assert(U == 8, "transpose_reduce8");
+    constexpr int UR = 4;  // gathers in flight (fewer registers, more warps)
     __shared__ double extra_s[kRowWarps][64];
     const int lane = lane_id();
     const int wi = threadIdx.x >> 5;
@@ -405,15 +437,15 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_gn_rows1(const GnArgs g, con
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const unsigned okm = cnt > 0 ? wd[h].okm : 0u;
-        for (int j0 = 0; j0 < 32; j0 += U) {
-            if (((okm >> j0) & ((1u << U) - 1u)) == 0) continue;
-            float x[U][VW];
-            double w[U];
-            bool valid[U];
-            gather<VW>(g, wd[h], j0, fl, lane_on, x, w, valid);
-            double part[U];
+        for (int j0 = 0; j0 < 32; j0 += UR) {
+            if (((okm >> j0) & ((1u << UR) - 1u)) == 0) continue;
+            float x[UR][VW];
+            double w[UR];
+            bool valid[UR];
+            gather<VW, UR>(g, wd[h], j0, fl, lane_on, x, w, valid);
+            double part[UR];
 #pragma unroll
-            for (int q = 0; q < U; ++q) {
+            for (int q = 0; q < UR; ++q) {
                 part[q] = 0.0;
 #pragma unroll
                 for (int e = 0; e < VW; ++e) {
@@ -429,9 +461,9 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_gn_rows1(const GnArgs g, con
                     }
                 }
             }
-            const double r = transpose_reduce8(part);
-            const double got = __shfl_sync(FG_FULL_MASK, r, reduce8_src((lane - j0) & 7));
-            if (lane >= j0 && lane < j0 + U) mine[h] = got;
+            const double r = transpose_reduce4(part);
+            const double got = __shfl_sync(FG_FULL_MASK, r, reduce4_src((lane - j0) & 3));
+            if (lane >= j0 && lane < j0 + UR) mine[h] = got;
         }
     }
     __syncwarp();
@@ -478,8 +510,12 @@ __global__ void k_gn_fill(const GnArgs g, const GnBwd bw) {
 // max-block gradient scattered to u), float64.  The sum over the list is
 // order-independent up to float64 rounding (the list order comes from the
 // atomic fill), far inside the float32 output precision.
+#ifndef FG_GN_COLS_U
+#define FG_GN_COLS_U 2
+#endif
 template <int VW>
 __global__ void __launch_bounds__(kRowWarps * 32) k_gn_cols(const GnArgs g, const GnBwd bw, int f0) {
+    constexpr int UC = FG_GN_COLS_U;
     const int lane = lane_id();
     const int64_t p = blockIdx.x * (int64_t)kRowWarps + (threadIdx.x >> 5);
     if (p >= g.n) return;
@@ -502,11 +538,11 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_gn_cols(const GnArgs g, cons
                 w = exp(-g.scale * (double)__ldg(&g.d2[t]));
             }
             const int nb = min(32, hi - base);
-            for (int j0 = 0; j0 < nb; j0 += U) {
-                float x[U][VW];
-                double wq[U];
+            for (int j0 = 0; j0 < nb; j0 += UC) {
+                float x[UC][VW];
+                double wq[UC];
 #pragma unroll
-                for (int q = 0; q < U; ++q) {
+                for (int q = 0; q < UC; ++q) {
                     const int32_t vq = __shfl_sync(FG_FULL_MASK, vv, (j0 + q) & 31);
                     wq[q] = __shfl_sync(FG_FULL_MASK, w, (j0 + q) & 31);
 #pragma unroll
@@ -514,7 +550,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_gn_cols(const GnArgs g, cons
                     if (j0 + q < nb && lane_on) ldf<VW>(bw.cm + (int64_t)vq * F + fl, x[q]);
                 }
 #pragma unroll
-                for (int q = 0; q < U; ++q) {
+                for (int q = 0; q < UC; ++q) {
 #pragma unroll
                     for (int e = 0; e < VW; ++e) acc[e] += wq[q] * (double)x[q][e];
                 }
