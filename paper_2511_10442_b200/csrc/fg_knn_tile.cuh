@@ -200,6 +200,28 @@ __device__ __forceinline__ QP pack_q(const float4 q) {
     return r;
 }
 
+// Predicated append of up to four candidate codes (d <= thr) to the lane's
+// list (one asm block: no register copies of the list pointer in between).
+__device__ __forceinline__ void append4(uint32_t& ptr, const float (&d)[4], float thr, uint32_t c0,
+                                        uint32_t c1, uint32_t c2, uint32_t c3) {
+    asm volatile(
+        "{ .reg .pred p0, p1, p2, p3;\n\t"
+        "setp.le.f32 p0, %1, %5;\n\t"
+        "setp.le.f32 p1, %2, %5;\n\t"
+        "setp.le.f32 p2, %3, %5;\n\t"
+        "setp.le.f32 p3, %4, %5;\n\t"
+        "@p0 st.shared.u16 [%0], %6;\n\t"
+        "@p0 add.u32 %0, %0, 2;\n\t"
+        "@p1 st.shared.u16 [%0], %7;\n\t"
+        "@p1 add.u32 %0, %0, 2;\n\t"
+        "@p2 st.shared.u16 [%0], %8;\n\t"
+        "@p2 add.u32 %0, %0, 2;\n\t"
+        "@p3 st.shared.u16 [%0], %9;\n\t"
+        "@p3 add.u32 %0, %0, 2; }"
+        : "+r"(ptr)
+        : "f"(d[0]), "f"(d[1]), "f"(d[2]), "f"(d[3]), "f"(thr), "r"(c0), "r"(c1), "r"(c2), "r"(c3));
+}
+
 // Four candidates of a chunk, SoA: x[dim] = (c_j, c_j+1), (c_j+2, c_j+3) pairs.
 struct G4 {
     unsigned long long x[4][2];
@@ -229,14 +251,7 @@ __device__ __forceinline__ void eval_g4(const G4& g, const QP& q, float tau, uin
         }
         asm("mov.b64 {%0, %1}, %2;" : "=f"(d[2 * h]), "=f"(d[2 * h + 1]) : "l"(acc));
     }
-    const uint32_t cs[4] = {c0, c1, c2, c3};
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-        asm volatile(
-            "{ .reg .pred p; setp.le.f32 p, %1, %2; @p st.shared.u16 [%0], %3; "
-            "@p add.u32 %0, %0, 2; }"
-            : "+r"(ptr)
-            : "f"(d[i]), "f"(tau), "r"(cs[i]));
+    append4(ptr, d, tau, c0, c1, c2, c3);
 }
 
 // Expanded form around the tile centre: d2 = |q'|^2 + |c'|^2 - 2 q'.c' with
@@ -246,6 +261,7 @@ __device__ __forceinline__ void eval_g4(const G4& g, const QP& q, float tau, uin
 struct QX {
     unsigned long long sq;      // (|q'|^2, |q'|^2)
     unsigned long long m2q[4];  // (-2 q'_d, -2 q'_d)
+    float tau_x;                // tau - |q'|^2: |c'|^2 - 2 q'.c' is compared with it
 };
 struct G4X {
     unsigned long long x[4][2];
@@ -261,55 +277,18 @@ __device__ __forceinline__ void load_g4x(G4X& g, uint32_t sx_addr, int j) {
                  : "=l"(g.n[0]), "=l"(g.n[1])
                  : "r"(sx_addr + 4 * 128 + j * 4));
 }
-__device__ __forceinline__ void eval_g4x(const G4X& g, const QX& q, float tau, uint32_t& ptr,
+__device__ __forceinline__ void eval_g4x(const G4X& g, const QX& q, float tau_x, uint32_t& ptr,
                                          uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3) {
     float d[4];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        unsigned long long acc;
-        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc) : "l"(g.n[h]), "l"(q.sq));
+    for (int h = 0; h < 2; ++h) {  // |c'|^2 - 2 q'.c' for a candidate pair: 4 FFMA2
+        unsigned long long acc = g.n[h];
 #pragma unroll
         for (int dd = 0; dd < 4; ++dd)
             asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(acc) : "l"(g.x[dd][h]), "l"(q.m2q[dd]), "l"(acc));
         asm("mov.b64 {%0, %1}, %2;" : "=f"(d[2 * h]), "=f"(d[2 * h + 1]) : "l"(acc));
     }
-    const uint32_t cs[4] = {c0, c1, c2, c3};
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-        asm volatile(
-            "{ .reg .pred p; setp.le.f32 p, %1, %2; @p st.shared.u16 [%0], %3; "
-            "@p add.u32 %0, %0, 2; }"
-            : "+r"(ptr)
-            : "f"(d[i]), "f"(tau), "r"(cs[i]));
-}
-
-__device__ __forceinline__ void eval_g8x(const G4X& g0, const G4X& g1, const QX& q, float tau,
-                                         uint32_t& ptr, const uint32_t* cs) {
-    float d[8];
-    unsigned long long acc[4];
-#pragma unroll
-    for (int h = 0; h < 4; ++h) {
-        const G4X& g = h < 2 ? g0 : g1;
-        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc[h]) : "l"(g.n[h & 1]), "l"(q.sq));
-    }
-#pragma unroll
-    for (int dd = 0; dd < 4; ++dd)
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-            const G4X& g = h < 2 ? g0 : g1;
-            asm("fma.rn.f32x2 %0, %1, %2, %3;"
-                : "=l"(acc[h]) : "l"(g.x[dd][h & 1]), "l"(q.m2q[dd]), "l"(acc[h]));
-        }
-#pragma unroll
-    for (int h = 0; h < 4; ++h)
-        asm("mov.b64 {%0, %1}, %2;" : "=f"(d[2 * h]), "=f"(d[2 * h + 1]) : "l"(acc[h]));
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-        asm volatile(
-            "{ .reg .pred p; setp.le.f32 p, %1, %2; @p st.shared.u16 [%0], %3; "
-            "@p add.u32 %0, %0, 2; }"
-            : "+r"(ptr)
-            : "f"(d[i]), "f"(tau), "r"(cs[i]));
+    append4(ptr, d, tau_x, c0, c1, c2, c3);
 }
 
 __device__ __forceinline__ unsigned long long pack2(float x) {
@@ -381,7 +360,7 @@ __device__ __forceinline__ void scan_tile(TileWarp& W, const float4* __restrict_
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 if (j + 1 < 8) load_g4x(gb[(j + 1) & 1], sx_addr, 4 * (j + 1));
-                eval_g4x(gb[j & 1], qx, tau, ptr, cd[4 * j], cd[4 * j + 1], cd[4 * j + 2],
+                eval_g4x(gb[j & 1], qx, qx.tau_x, ptr, cd[4 * j], cd[4 * j + 1], cd[4 * j + 2],
                          cd[4 * j + 3]);
             }
         } else {
@@ -834,6 +813,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_tile_search(const __grid_con
         qx.m2q[1] = pack2(-2.0f * qs.y);
         qx.m2q[2] = pack2(-2.0f * qs.z);
         qx.m2q[3] = pack2(-2.0f * qs.w);
+        qx.tau_x = tau - sq;
         st_exp += expanded ? 1 : 0;
         if (expanded)
             scan_tile<true>(W, a.sc, T, nsp, qv, qx, cen, tau, ptr, overflow, llim);
