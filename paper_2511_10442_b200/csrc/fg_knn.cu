@@ -19,11 +19,16 @@ constexpr int kStatsTotal = ST_COUNT + tile::TS_COUNT;
 
 // The lane-per-query tile path (fg_knn_tile.cuh) serves every coordinate
 // binned, d <= 4, k - 1 <= 40, no mask / radius / exhaustive / float64 output.
-bool tile_path(int32_t n_coords, int32_t d_bin, int32_t n_bins, int32_t k, uint32_t flags) {
+bool tile_path(int32_t n_coords, int32_t n_splits, int32_t d_bin, int32_t n_bins, int32_t k,
+               uint32_t flags) {
     const uint32_t off = FG_KNN_USE_DIRECTION | FG_KNN_USE_MAX_R2 | FG_KNN_EXHAUSTIVE |
                          FG_KNN_D2_F64 | FG_KNN_NO_TILE;
-    return n_coords == d_bin && n_coords <= 4 && n_bins <= 32 && k >= 2 &&
-           k - 1 <= tile::kMaxNeed && !(flags & off);
+    if (!(n_coords == d_bin && n_coords <= 4 && n_bins <= 32 && k >= 2 &&
+          k - 1 <= tile::kMaxNeed && !(flags & off)))
+        return false;
+    int64_t blocks = n_splits;  // lead blocks must fit the int32 tile descriptors
+    for (int i = 0; i < d_bin - 1; ++i) blocks *= (n_bins + 1) / 2;
+    return blocks < ((int64_t)1 << 30);
 }
 
 // Argument validation shared by both entry points (before any CUDA call).
@@ -63,7 +68,8 @@ TileWs tile_ws(void* base, int64_t n, int32_t n_splits, int32_t d_bin, int32_t n
     int64_t bps = 1;
     for (int i = 0; i < d_bin - 1; ++i) bps *= nblk;
     w.n_blocks = bps * n_splits;
-    const int64_t max_tiles = w.n_blocks * n_bins;
+    // a tile holds >= 1 point: at most min(blocks x columns, n) tiles
+    const int64_t max_tiles = std::min<int64_t>(w.n_blocks * n_bins, std::max<int64_t>(n, 1));
     char* p = static_cast<char*>(base);
     size_t off = 0;
     w.ctr = reinterpret_cast<int*>(p + off);
@@ -81,7 +87,7 @@ extern "C" int fg_knn_workspace_size(int64_t n, int32_t n_coords, int32_t n_spli
                                      int32_t n_bins, int32_t k, uint32_t flags, size_t* bytes) {
     if (!bytes) return FG_ERR_NULL;
     if (n < 0 || n_splits < 1 || n_bins < 1) return FG_ERR_BAD_SHAPE;
-    *bytes = tile_path(n_coords, d_bin, n_bins, k, flags)
+    *bytes = tile_path(n_coords, n_splits, d_bin, n_bins, k, flags)
                  ? tile_ws(nullptr, n, n_splits, d_bin, n_bins).bytes
                  : 0;
     return 0;
@@ -99,7 +105,7 @@ extern "C" int fg_knn_fwd(const float* sorted_coords, const int32_t* sort_order,
                       out_idx, out_d2));
     if (n == 0) return 0;
     size_t bytes = 0;
-    if (tile_path(n_coords, d_bin, n_bins, k, flags))
+    if (tile_path(n_coords, n_splits, d_bin, n_bins, k, flags))
         bytes = tile_ws(nullptr, n, n_splits, d_bin, n_bins).bytes;
     void* ws = nullptr;
     cudaStream_t st = (cudaStream_t)stream;
@@ -155,7 +161,7 @@ extern "C" int fg_knn_fwd_ws(const float* sorted_coords, const int32_t* sort_ord
         a.stats = g_stats_dev;
     }
     cudaStream_t st = (cudaStream_t)stream;
-    if (tile_path(n_coords, d_bin, n_bins, k, flags)) {
+    if (tile_path(n_coords, n_splits, d_bin, n_bins, k, flags)) {
         const TileWs w = tile_ws(workspace, n, n_splits, d_bin, n_bins);
         if (!workspace) return FG_ERR_NULL;
         if (workspace_bytes < w.bytes) return FG_ERR_WORKSPACE;
