@@ -423,15 +423,12 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_gn_rows1(const GnArgs g, con
         for (int e = 0; e < VW; ++e) o[e] = (float)cmean[e];
         stf<VW>(bw.cm + v * F + fl, o);
     }
-    double best[VW], bwt[VW];
-    float bx[VW];
+    double best[VW];
     int bslot[VW];
 #pragma unroll
     for (int e = 0; e < VW; ++e) {
         best[e] = -INFINITY;
         bslot[e] = -1;
-        bwt[e] = 0.0;
-        bx[e] = 0.0f;
     }
     double mine[2] = {0.0, 0.0};  // this lane's slot: mean-block dot product
 #pragma unroll
@@ -455,8 +452,6 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_gn_rows1(const GnArgs g, con
                         if (term > best[e]) {
                             best[e] = term;
                             bslot[e] = 32 * h + j0 + q;
-                            bwt[e] = w[q];
-                            bx[e] = x[q][e];
                         }
                     }
                 }
@@ -468,15 +463,18 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_gn_rows1(const GnArgs g, con
     }
     __syncwarp();
     // max blocks: slot bslot gets -scale w x cmax in grad_d2, neighbour u gets w cmax
+    // (w and x at the arg-max are re-read: L1 hits, no per-element bookkeeping)
     if (has_max && lane_on && cnt > 0) {
 #pragma unroll
         for (int e = 0; e < VW; ++e) {
             if (bslot[e] < 0) continue;
-            atomicAdd(&extra_s[wi][bslot[e]], (double)bx[e] * cmax[e]);
-            if (bw.gmax) {
-                const int32_t u = __ldg(&g.idx[v * k + bslot[e]]);
-                atomicAdd(&bw.gmax[(int64_t)u * F + fl + e], bwt[e] * cmax[e]);
-            }
+            const int32_t u = __ldg(&g.idx[v * k + bslot[e]]);
+            const double wb = exp(-g.scale * (double)__ldg(&g.d2[v * k + bslot[e]]));
+            const float xb = __ldg(&g.feats[(int64_t)u * F + fl + e]);
+            atomicAdd(&extra_s[wi][bslot[e]], (double)xb * cmax[e]);
+#ifndef FG_GN_NO_GMAX  // timing experiment only
+            if (bw.gmax) atomicAdd(&bw.gmax[(int64_t)u * F + fl + e], wb * cmax[e]);
+#endif
         }
     }
     __syncwarp();
