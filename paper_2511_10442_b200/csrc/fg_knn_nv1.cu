@@ -22,7 +22,7 @@ int launch_db(TileArgs& t, const search::KnnArgs& a, cudaStream_t st) {
                                      (int)tile_smem_bytes()));
         FG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     }
-    k_tile_search<DB><<<(unsigned)(sms * 4), kWarps * 32, tile_smem_bytes(), st>>>(t);
+    k_tile_search<DB><<<(unsigned)(sms * kCtasPerSm), kWarps * 32, tile_smem_bytes(), st>>>(t);
     FG_TRY(launched(st));
     // whatever the tiles could not certify: the warp-per-query kernel
     search::KnnArgs r = a;

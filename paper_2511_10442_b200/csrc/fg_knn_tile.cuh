@@ -47,12 +47,19 @@ namespace tile {
 
 constexpr int kWarps = 4;          // warps per CTA (4 CTAs per SM: 16 warps)
 constexpr int kCap = 88;           // list entries per lane
-constexpr int kSlack = 32;         // one chunk of overrun before the clamp
-constexpr int kStride = kCap + kSlack + 2;  // u16 per lane list: 61 words, odd -> bank spread
-constexpr int kBkt = 256;          // epilogue buckets (8 per lane)
+constexpr int kSlack = 16;         // half a chunk of overrun before the clamp
+constexpr int kStride = kCap + kSlack + 2;  // u16 per lane list: 53 words, odd -> bank spread
+#ifndef FG_TILE_CTAS
+#define FG_TILE_CTAS 4
+#endif
+constexpr int kCtasPerSm = FG_TILE_CTAS;
+constexpr int kBkt = 128;          // epilogue buckets (4 per lane)
 constexpr int kMaxSpans = 320;     // candidate spans per tile
 constexpr int kMaxSpanLen = 127;   // 7-bit offsets in the codes
-constexpr float kAlpha = 1.12f;    // radius inflation over the density estimate
+#ifndef FG_TILE_ALPHA
+#define FG_TILE_ALPHA 1.10f
+#endif
+constexpr float kAlpha = FG_TILE_ALPHA;  // radius inflation over the density estimate
 constexpr float kMargin = 1.0f + 1e-5f;
 constexpr float kSlackCells = 1e-4f;
 constexpr float kInf = __builtin_huge_valf();
@@ -93,6 +100,8 @@ struct TileWarp {
 };
 
 __host__ __device__ constexpr size_t tile_smem_bytes() { return sizeof(TileWarp) * kWarps; }
+static_assert(tile_smem_bytes() * kCtasPerSm + 1024 * kCtasPerSm <= 233472,
+              "k_tile_search: CTAs per SM do not fit in shared memory");
 
 // Lead block `b` of a split -> origin cells (last lead dim fastest).
 template <int NL>
@@ -362,6 +371,10 @@ __device__ __forceinline__ void scan_tile(TileWarp& W, const float4* __restrict_
                 if (j + 1 < 8) load_g4x(gb[(j + 1) & 1], sx_addr, 4 * (j + 1));
                 eval_g4x(gb[j & 1], qx, qx.tau_x, ptr, cd[4 * j], cd[4 * j + 1], cd[4 * j + 2],
                          cd[4 * j + 3]);
+                if (j == 3 && ptr > llim) {  // clamp every 16 candidates (kSlack)
+                    overflow = true;
+                    ptr = llim;
+                }
             }
         } else {
             // direct form (the ~10% of tiles the expanded bound rejects): rolled, small code
@@ -371,6 +384,10 @@ __device__ __forceinline__ void scan_tile(TileWarp& W, const float4* __restrict_
                 load_g4(gq, sx_addr, 4 * j);
                 const uint4 cv = reinterpret_cast<const uint4*>(W.scode)[j];
                 eval_g4(gq, qv, tau, ptr, cv.x, cv.y, cv.z, cv.w);
+                if (j == 3 && ptr > llim) {
+                    overflow = true;
+                    ptr = llim;
+                }
             }
         }
         if (ptr > llim) {
@@ -488,8 +505,7 @@ __device__ __forceinline__ bool finish_query(TileWarp& W, const TileArgs& a, int
     }
     if (__reduce_add_sync(FG_FULL_MASK, n_in) < need) return false;
     // counting sort by bucket: counts (match_any groups + one smem atomic per group)
-    *reinterpret_cast<uint4*>(&W.bcnt[8 * lane]) = make_uint4(0u, 0u, 0u, 0u);
-    *reinterpret_cast<uint4*>(&W.bcnt[8 * lane + 4]) = make_uint4(0u, 0u, 0u, 0u);
+    *reinterpret_cast<uint4*>(&W.bcnt[4 * lane]) = make_uint4(0u, 0u, 0u, 0u);
     __syncwarp();
     int bk[R], idx[R];
 #pragma unroll
@@ -506,25 +522,19 @@ __device__ __forceinline__ bool finish_query(TileWarp& W, const TileArgs& a, int
         }
     }
     __syncwarp();
-    uint4 ca = *reinterpret_cast<const uint4*>(&W.bcnt[8 * lane]);
-    uint4 cb = *reinterpret_cast<const uint4*>(&W.bcnt[8 * lane + 4]);
-    const unsigned tot = ca.x + ca.y + ca.z + ca.w + cb.x + cb.y + cb.z + cb.w;
+    uint4 ca = *reinterpret_cast<const uint4*>(&W.bcnt[4 * lane]);
+    const unsigned tot = ca.x + ca.y + ca.z + ca.w;
     const unsigned incl = warp_inclusive_scan(tot);
     const int n_valid = (int)__shfl_sync(FG_FULL_MASK, incl, 31);
     __syncwarp();
-    {  // exclusive starts of this lane's 8 buckets
+    {  // exclusive starts of this lane's 4 buckets
         unsigned run = incl - tot, t0;
         t0 = ca.x; ca.x = run; run += t0;
         t0 = ca.y; ca.y = run; run += t0;
         t0 = ca.z; ca.z = run; run += t0;
-        t0 = ca.w; ca.w = run; run += t0;
-        t0 = cb.x; cb.x = run; run += t0;
-        t0 = cb.y; cb.y = run; run += t0;
-        t0 = cb.z; cb.z = run; run += t0;
-        cb.w = run;
+        ca.w = run;
     }
-    *reinterpret_cast<uint4*>(&W.bcnt[8 * lane]) = ca;
-    *reinterpret_cast<uint4*>(&W.bcnt[8 * lane + 4]) = cb;
+    *reinterpret_cast<uint4*>(&W.bcnt[4 * lane]) = ca;
     if (lane == 31) W.bcnt[kBkt] = incl;
     __syncwarp();
 #pragma unroll
@@ -591,7 +601,7 @@ __device__ __forceinline__ bool finish_query(TileWarp& W, const TileArgs& a, int
 
 // ---------------------------------------------------------------- search
 template <int DB>
-__global__ void __launch_bounds__(kWarps * 32, 4) k_tile_search(const __grid_constant__ TileArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) k_tile_search(const __grid_constant__ TileArgs a) {
     constexpr int NL = DB - 1;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TileWarp& W = reinterpret_cast<TileWarp*>(smem_raw)[threadIdx.x >> 5];
