@@ -710,8 +710,16 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) k_tile_search(const _
                                (1.0f / (float)DB));
         // per-lane radius corrected for the part of the ball outside the grid
         float rad = kAlpha * rk;
+        // only lanes within reach of a face of the grid box need the correction
+        // (a radius <= 3 r_k: the ball of the first iteration can grow by f^(-1/d))
+        bool near_face = false;
+#pragma unroll
+        for (int i = 0; i < DB; ++i) {
+            const float h0 = qa[i] - mn[i];
+            near_face |= fminf(h0, (float)nb * w[i] - h0) < 3.0f * rad;
+        }
 #pragma unroll 1
-        for (int it = 0; it < 3; ++it) {
+        for (int it = 0; it < (__any_sync(FG_FULL_MASK, active && near_face) ? 3 : 0); ++it) {
             float f = 1.0f;
 #pragma unroll
             for (int i = 0; i < DB; ++i) {
