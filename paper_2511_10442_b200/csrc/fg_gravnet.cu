@@ -172,6 +172,77 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_gn_fwd(const GnArgs g, int f
     }
 }
 
+// Half-warp slot pairs (F % 4 == 0, F <= 64): lanes 0-15 take slot j, lanes
+// 16-31 slot j+1, each lane 4 features (one 16-byte gather), so the per-slot
+// bookkeeping (neighbour id / weight shuffles, validity, address) is paid by
+// half the lanes per feature; the two halves are combined at the end.
+#ifndef FG_GN_PAIRS_U
+#define FG_GN_PAIRS_U 2
+#endif
+
+template <int UP>
+__global__ void __launch_bounds__(kRowWarps * 32) k_gn_fwd_pairs(const GnArgs g, float* __restrict__ out) {
+    const int lane = lane_id();
+    const int64_t p = blockIdx.x * (int64_t)kRowWarps + (threadIdx.x >> 5);
+    if (p >= g.n) return;
+    const int64_t v = row_of(g, p);
+    const int k = g.k, F = g.F, W = F * g.n_red;
+    const int half = lane >> 4;
+    const int fl = (lane & 15) * 4;
+    const bool lane_on = fl < F;
+    double sum[4], mx[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        sum[e] = 0.0;
+        mx[e] = -INFINITY;
+    }
+    int cnt = 0;
+    for (int base = 0; base < k; base += 32) {
+        const Window wd = load_window(g, v, base, true);
+        cnt += __popc(wd.okm);
+        for (int j0 = 0; j0 < 32; j0 += 2 * UP) {
+            if (((wd.okm >> j0) & ((1u << (2 * UP)) - 1u)) == 0) continue;
+            float4 x[UP];
+            double w[UP];
+            bool valid[UP];
+#pragma unroll
+            for (int q = 0; q < UP; ++q) {
+                const int jj = j0 + 2 * q + half;
+                valid[q] = (wd.okm >> jj) & 1u;
+                const int32_t uq = __shfl_sync(FG_FULL_MASK, wd.u, jj);
+                w[q] = __shfl_sync(FG_FULL_MASK, wd.w, jj);
+                x[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (valid[q] && lane_on)
+                    x[q] = __ldg(reinterpret_cast<const float4*>(g.feats + (int64_t)uq * F + fl));
+            }
+#pragma unroll
+            for (int q = 0; q < UP; ++q) {
+                if (!valid[q]) continue;
+                const float xe[4] = {x[q].x, x[q].y, x[q].z, x[q].w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const double term = w[q] * (double)xe[e];
+                    sum[e] += term;
+                    mx[e] = term > mx[e] ? term : mx[e];
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        sum[e] += __shfl_xor_sync(FG_FULL_MASK, sum[e], 16);
+        const double om = __shfl_xor_sync(FG_FULL_MASK, mx[e], 16);
+        mx[e] = om > mx[e] ? om : mx[e];  // the value; which slot holds it does not matter here
+    }
+    if (half || !lane_on) return;
+    for (int b = 0; b < g.n_red; ++b) {
+        float o[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) o[e] = cnt > 0 ? (float)(is_max(g, b) ? mx[e] : sum[e] / (double)cnt) : 0.0f;
+        *reinterpret_cast<float4*>(out + v * W + (int64_t)b * F + fl) = make_float4(o[0], o[1], o[2], o[3]);
+    }
+}
+
 // ---------------------------------------------------------------- backward
 struct GnBwd {
     const float* up;      // (n, F * n_red)
@@ -681,6 +752,10 @@ extern "C" int fg_gravnet_fwd(const float* feats, int64_t n, int32_t n_feats, co
     g.scale = weight_scale; g.include_self = include_self; g.order = order;
     cudaStream_t st = (cudaStream_t)stream;
     const unsigned blocks = (unsigned)ceil_div(n, kRowWarps);
+    if (n_feats % 4 == 0 && n_feats <= 64 && ((uintptr_t)feats % 16) == 0 && ((uintptr_t)out % 16) == 0) {
+        k_gn_fwd_pairs<FG_GN_PAIRS_U><<<blocks, kRowWarps * 32, 0, st>>>(g, out);
+        return launched(st);
+    }
     return with_vw(pick_vw(n_feats, {feats, out}), [&](auto vw) {
         constexpr int VW = decltype(vw)::value;
         for (int f0 = 0; f0 < n_feats; f0 += 32 * VW) {
