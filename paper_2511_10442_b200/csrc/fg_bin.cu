@@ -360,7 +360,7 @@ int launch_bin_core(const float* coords, int64_t n, int n_c, const int64_t* rs, 
     k_bbox_init<<<(unsigned)ceil_div(m, 256), 256, 0, st>>>(w.bbox, m);
     FG_TRY(launched(st));
     if (n > 0) {
-        const int64_t chunk = 8192;
+        const int64_t chunk = 2048;
         k_bbox<DB><<<(unsigned)ceil_div(n, chunk), 256, 0, st>>>(coords, n, n_c, rs, n_splits,
                                                                  chunk, w.bbox);
         FG_TRY(launched(st));
