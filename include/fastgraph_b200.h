@@ -162,6 +162,24 @@ int fg_gravnet_fwd(const float *feats, int64_t n, int32_t n_feats, const int32_t
 
 int fg_gravnet_bwd_workspace_size(int64_t n, int32_t n_feats, int32_t k, size_t *bytes);
 
+/* Fused search + GravNet aggregation (the fusion the paper
+ * describes): binned_select_knn (float32 distances, no mask /
+ * radius) and gravnet_aggregate of its rows in one pass -- the tile path
+ * aggregates every row it writes straight from its staged row, the rows it
+ * leaves to the warp-per-query kernel are aggregated afterwards.  Outputs are
+ * those of fg_knn_fwd_ws + fg_gravnet_fwd (scratch: fg_knn_workspace_size with
+ * the same flags).  Falls back to exactly that pair when the tile path does
+ * not apply or F is odd or > 64. */
+int fg_knn_gravnet_fwd_ws(const float *sorted_coords, const int32_t *sort_order,
+                          const int64_t *bin_idx, const int32_t *bin_bounds,
+                          const int64_t *row_splits, const double *dim_mins, const double *widths,
+                          int64_t n, int32_t n_coords, int32_t n_splits, int32_t d_bin,
+                          int32_t n_bins, int32_t k, uint32_t flags, const float *feats,
+                          int32_t n_feats, double weight_scale, const int32_t *reducers,
+                          int32_t n_reducers, int32_t include_self, int32_t *out_idx,
+                          float *out_d2, float *agg_out, void *workspace, size_t workspace_bytes,
+                          void *stream);
+
 /* gravnet_aggregate_backward.  Replaces G/gravnet.py:100-150 ->
  * (grad_feats[n,F] float32, grad_d2[n,k] float32); max blocks route to the
  * lowest arg-max slot.  grad_d2 comes from a row pass, grad_feats from a pass

@@ -32,6 +32,7 @@ EXPORTS = (
     "fg_knn_bwd_workspace_size", "fg_knn_bwd", "fg_gravnet_fwd",
     "fg_gravnet_bwd_workspace_size", "fg_gravnet_bwd", "fg_error_string", "fg_abi_version",
     "fg_launch_count", "fg_knn_stats", "fg_knn_workspace_size", "fg_knn_fwd_ws",
+    "fg_knn_gravnet_fwd_ws",
 )
 
 _P = ctypes.c_void_p
@@ -51,6 +52,9 @@ _SIGS = {
     "fg_knn_workspace_size": ([_I64, _I32, _I32, _I32, _I32, _I32, _U32, _SZ], ctypes.c_int),
     "fg_knn_fwd_ws": ([_P, _P, _P, _P, _P, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _P, _D,
                        _U32, _P, _P, _P, ctypes.c_size_t, _P], ctypes.c_int),
+    "fg_knn_gravnet_fwd_ws": ([_P, _P, _P, _P, _P, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32,
+                               _U32, _P, _I32, _D, _P, _I32, _I32, _P, _P, _P, _P,
+                               ctypes.c_size_t, _P], ctypes.c_int),
     "fg_knn_bwd_workspace_size": ([_I64, _I32, _SZ], ctypes.c_int),
     "fg_knn_bwd": ([_P, _I64, _I32, _P, _I32, _P, _P, _P, _I32, _P, ctypes.c_size_t, _P],
                    ctypes.c_int),

@@ -10,6 +10,13 @@ namespace fg {
 namespace tile {
 int launch(TileArgs& t, const search::KnnArgs& a, int d_bin, cudaStream_t st);
 }
+namespace gravnet {
+int launch_fwd_list(const float* feats, int64_t n, int F, const int32_t* idx, const float* d2, int k,
+                    double scale, const int32_t* reducers, int n_red, int include_self,
+                    const int32_t* plist, const int* pcount, const int32_t* psid, float* out,
+                    cudaStream_t st);
+int reducer_bits(const int32_t* reducers, int n_red, unsigned* bits);
+}  // namespace gravnet
 }  // namespace fg
 
 namespace {
@@ -53,6 +60,18 @@ int check_args(const float* sorted_coords, const int32_t* sort_order, const int6
     if ((flags & FG_KNN_USE_DIRECTION) && !dir_mask) return FG_ERR_NULL;
     return 0;
 }
+
+// Fused GravNet request for the current call (set by fg_knn_gravnet_fwd_ws
+// around its call of fg_knn_fwd_ws; thread-local, so concurrent host threads
+// do not interfere).
+struct FusedGn {
+    const float* feats;
+    float* out;
+    int F, n_red, include_self;
+    unsigned max_bits;
+    double scale;
+};
+thread_local const FusedGn* g_fused = nullptr;
 
 struct TileWs {
     int* ctr;
@@ -165,7 +184,16 @@ extern "C" int fg_knn_fwd_ws(const float* sorted_coords, const int32_t* sort_ord
         const TileWs w = tile_ws(workspace, n, n_splits, d_bin, n_bins);
         if (!workspace) return FG_ERR_NULL;
         if (workspace_bytes < w.bytes) return FG_ERR_WORKSPACE;
-        tile::TileArgs t;
+        tile::TileArgs t{};
+        if (g_fused) {  // fg_knn_gravnet_fwd_ws: aggregate every row the tiles write
+            t.gn_feats = g_fused->feats;
+            t.gn_out = g_fused->out;
+            t.gn_F = g_fused->F;
+            t.gn_n_red = g_fused->n_red;
+            t.gn_incl = g_fused->include_self;
+            t.gn_max_bits = g_fused->max_bits;
+            t.gn_scale = g_fused->scale;
+        }
         t.sc = a.sc;
         t.sid = sort_order;
         t.bounds = bin_bounds;
@@ -202,4 +230,49 @@ extern "C" int fg_knn_stats(uint64_t* out, int32_t n, int32_t reset) {
     }
     for (int i = 0; i < n && i < kStatsTotal; ++i) out[i] = h[i];
     return 0;
+}
+
+extern "C" int fg_knn_gravnet_fwd_ws(const float* sorted_coords, const int32_t* sort_order,
+                                     const int64_t* bin_idx, const int32_t* bin_bounds,
+                                     const int64_t* row_splits, const double* dim_mins,
+                                     const double* widths, int64_t n, int32_t n_coords,
+                                     int32_t n_splits, int32_t d_bin, int32_t n_bins, int32_t k,
+                                     uint32_t flags, const float* feats, int32_t n_feats,
+                                     double weight_scale, const int32_t* reducers,
+                                     int32_t n_reducers, int32_t include_self, int32_t* out_idx,
+                                     float* out_d2, float* agg_out, void* workspace,
+                                     size_t workspace_bytes, void* stream) {
+    // the fused op always returns float32 distances, no mask / radius
+    if (flags & (FG_KNN_D2_F64 | FG_KNN_USE_DIRECTION | FG_KNN_USE_MAX_R2)) return FG_ERR_BAD_SHAPE;
+    FG_TRY(check_args(sorted_coords, sort_order, bin_idx, bin_bounds, row_splits, dim_mins, widths,
+                      n, n_coords, n_splits, d_bin, n_bins, k, nullptr, 0.0, flags, out_idx,
+                      out_d2));
+    if (n_feats < 1 || !(weight_scale > 0.0)) return FG_ERR_BAD_SHAPE;
+    unsigned bits = 0;
+    FG_TRY(fg::gravnet::reducer_bits(reducers, n_reducers, &bits));
+    if (n == 0) return 0;
+    if (!feats || !agg_out) return FG_ERR_NULL;
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool fuse = tile_path(n_coords, n_splits, d_bin, n_bins, k, flags) && n_feats % 2 == 0 &&
+                      n_feats <= 64 && ((uintptr_t)feats % 8) == 0 && ((uintptr_t)agg_out % 8) == 0;
+    if (!fuse) {  // unfused: the search, then the aggregation (same results)
+        FG_TRY(fg_knn_fwd_ws(sorted_coords, sort_order, bin_idx, bin_bounds, row_splits, dim_mins,
+                             widths, n, n_coords, n_splits, d_bin, n_bins, k, nullptr, 0.0, flags,
+                             out_idx, out_d2, workspace, workspace_bytes, stream));
+        return fg_gravnet_fwd(feats, n, n_feats, out_idx, out_d2, k, weight_scale, reducers,
+                              n_reducers, include_self, sort_order, agg_out, stream);
+    }
+    FusedGn fg_req{feats, agg_out, n_feats, n_reducers, include_self, bits, weight_scale};
+    g_fused = &fg_req;
+    const int rc = fg_knn_fwd_ws(sorted_coords, sort_order, bin_idx, bin_bounds, row_splits,
+                                 dim_mins, widths, n, n_coords, n_splits, d_bin, n_bins, k,
+                                 nullptr, 0.0, flags, out_idx, out_d2, workspace, workspace_bytes,
+                                 stream);
+    g_fused = nullptr;
+    FG_TRY(rc);
+    // rows the tiles left to the warp-per-query kernel: aggregate them now
+    const TileWs w = tile_ws(workspace, n, n_splits, d_bin, n_bins);
+    return fg::gravnet::launch_fwd_list(feats, n, n_feats, out_idx, out_d2, k, weight_scale,
+                                        reducers, n_reducers, include_self, w.redo, &w.ctr[2],
+                                        sort_order, agg_out, st);
 }

@@ -321,3 +321,69 @@ def _gn_backward(ctx, grad_out):
 
 
 gravnet_aggregate.register_autograd(_gn_backward, setup_context=_gn_setup)
+
+
+# ---------------------------------------------------------------- fused search + GravNet
+@torch.library.custom_op(f"{_LIB_NS}::knn_gravnet", mutates_args=())
+def knn_gravnet(coords: Tensor, row_splits: Tensor, bin_idx: Tensor, sort_order: Tensor,
+                bin_bounds: Tensor, dim_mins: Tensor, widths: Tensor, sorted_coords: Tensor,
+                K: int, d_bin: int, n_bins: int, feats: Tensor, weight_scale: float,
+                reducers: list[int], include_self: bool) -> tuple[Tensor, Tensor, Tensor]:
+    """binned_select_knn (float32 distances) + gravnet_aggregate of its rows in one
+    pass: -> (idx, d2, aggregated features).  Same values as
+    the two ops in sequence; differentiable w.r.t. coords and feats."""
+    _require_cuda(coords, sorted_coords, feats)
+    L = _lib.load()
+    dev = sorted_coords.device
+    n, n_c = coords.shape
+    if feats.shape[0] != n:
+        raise ShapeMismatchError(f"{feats.shape[0]} feature rows for {n} vertices")
+    rs = row_splits.to(device=dev, dtype=torch.int64).contiguous()
+    S = rs.numel() - 1
+    F = feats.shape[1]
+    f = feats.to(torch.float32).contiguous()
+    red = _check_red(reducers)
+    flags = _DEBUG_FLAGS
+    idx = torch.empty((n, K), dtype=torch.int32, device=dev)
+    d2 = torch.empty((n, K), dtype=torch.float32, device=dev)
+    agg = torch.empty((n, F * red.numel()), dtype=torch.float32, device=dev)
+    nbytes = _lib.size_out(L.fg_knn_workspace_size, n, n_c, S, d_bin, n_bins, K, flags)
+    ws = _ws(nbytes, dev)
+    _lib.check(L.fg_knn_gravnet_fwd_ws(
+        _p(sorted_coords), _p(sort_order), _p(bin_idx), _p(bin_bounds), _p(rs), _p(dim_mins),
+        _p(widths), n, n_c, S, d_bin, n_bins, K, flags, _p(f), F, float(weight_scale),
+        ctypes.c_void_p(red.data_ptr()), red.numel(), int(include_self), _p(idx), _p(d2),
+        _p(agg), _p(ws), ws.numel(), _stream(sorted_coords)), "knn_gravnet")
+    return idx, d2, agg
+
+
+@knn_gravnet.register_fake
+def _kg_fake(coords, row_splits, bin_idx, sort_order, bin_bounds, dim_mins, widths, sorted_coords,
+             K, d_bin, n_bins, feats, weight_scale, reducers, include_self):
+    n = coords.shape[0]
+    return (coords.new_empty((n, K), dtype=torch.int32),
+            coords.new_empty((n, K), dtype=torch.float32),
+            feats.new_empty((n, feats.shape[1] * len(reducers)), dtype=torch.float32))
+
+
+def _kg_setup(ctx, inputs, output):
+    coords, order, feats = inputs[0], inputs[3], inputs[11]
+    ctx.save_for_backward(coords, output[0], output[1], feats, order)
+    ctx.args = (inputs[12], list(inputs[13]), inputs[14])
+    ctx.dtypes = (coords.dtype, feats.dtype)
+
+
+def _kg_backward(ctx, grad_idx, grad_d2, grad_agg):
+    coords, idx, d2, feats, order = ctx.saved_tensors
+    scale, reducers, include_self = ctx.args
+    gd, gf = grad_d2, None
+    if grad_agg is not None:
+        gf, gd_agg = gravnet_aggregate_grad(grad_agg, feats, idx, d2, scale, reducers,
+                                            include_self, order)
+        gd = gd_agg if gd is None else gd + gd_agg
+        gf = gf.to(ctx.dtypes[1])
+    gc = None if gd is None else binned_select_knn_grad(gd, idx, coords, order).to(ctx.dtypes[0])
+    return (gc,) + (None,) * 10 + (gf, None, None, None)
+
+
+knn_gravnet.register_autograd(_kg_backward, setup_context=_kg_setup)

@@ -87,3 +87,61 @@ def test_tile_equals_warp_kernel_full_size(cfg):
     assert np.array_equal(d0.view(np.uint32), d1.view(np.uint32))
     if cfg != "A":  # uniform 1M / 500k: the tile path certifies >= 99.5% of rows
         assert st["tile_redo"] < 0.005 * len(c), st
+
+
+# ---------------------------------------------------------------- fused search + GravNet
+def _fused_and_pair(c32, off, k, F, reducers, incl, seed=0):
+    n, d = c32.shape
+    nb = fg.compute_n_bins(int(np.diff(off).max()), k, d)
+    ct = torch.from_numpy(np.ascontiguousarray(c32)).cuda()
+    rs = torch.from_numpy(np.asarray(off, np.int64)).cuda()
+    bi, so, bb, mi, wi, sc = ops.bin_by_coordinates(ct, rs, d, nb)
+    feats = torch.from_numpy(np.random.default_rng(seed).standard_normal((n, F))
+                             .astype(np.float32)).cuda()
+    i1, d1, a1 = ops.knn_gravnet(ct, rs, bi, so, bb, mi, wi, sc, k, d, nb, feats, 10.0, reducers,
+                                 incl)
+    i0, d0 = ops.binned_select_knn(ct, rs, bi, so, bb, mi, wi, sc, k, d, nb, None, None, False,
+                                   False)
+    a0 = ops.gravnet_aggregate(feats, i0, d0, 10.0, reducers, incl, so)
+    torch.cuda.synchronize()
+    return (i0, d0, a0), (i1, d1, a1), feats
+
+
+@pytest.mark.parametrize("F,reducers,incl", [(64, [0, 1], True), (32, [1], False), (8, [0], True),
+                                            (65, [0, 1], True)])
+def test_fused_knn_gravnet_equals_ops(oracle, F, reducers, incl):
+    c, off = generate_dataset(20_000, 4, 2, 11, "uniform")
+    (i0, d0, a0), (i1, d1, a1), feats = _fused_and_pair(c.astype(np.float32), off, 40, F, reducers,
+                                                        incl)
+    assert torch.equal(i0, i1) and torch.equal(d0, d1)
+    np.testing.assert_allclose(a1.cpu().numpy(), a0.cpu().numpy(), rtol=1e-6, atol=1e-7)
+    names = ["mean" if r == 0 else "max" for r in reducers]
+    o = oracle.gravnet_aggregate(feats.cpu().numpy(), i1.cpu().numpy(), d1.cpu().numpy(), 10.0,
+                                 tuple(names), incl)
+    np.testing.assert_allclose(a1.cpu().numpy(), o, rtol=1e-5, atol=1e-6)
+
+
+def test_fused_knn_gravnet_full_size_and_grad():
+    c, off, k = config_dataset("E")
+    (i0, d0, a0), (i1, d1, a1), feats = _fused_and_pair(c, off, k, 64, [0, 1], True)
+    assert torch.equal(i0, i1) and torch.equal(d0, d1)
+    np.testing.assert_allclose(a1.cpu().numpy(), a0.cpu().numpy(), rtol=1e-6, atol=1e-7)
+    # autograd: the fused op's gradients = those of the two ops in sequence
+    n, d = c.shape
+    nb = fg.compute_n_bins(int(np.diff(off).max()), k, d)
+    ct = torch.from_numpy(c[:50_000].copy()).cuda().requires_grad_(True)
+    rs = torch.tensor([0, 50_000], dtype=torch.int64, device="cuda")
+    f = feats[:50_000].clone().requires_grad_(True)
+    bi, so, bb, mi, wi, sc = ops.bin_by_coordinates(ct.detach(), rs, d, nb)
+    up = torch.randn(50_000, 128, device="cuda")
+    _, d2f, af = ops.knn_gravnet(ct, rs, bi, so, bb, mi, wi, sc, k, d, nb, f, 10.0, [0, 1], True)
+    (af * up).sum().backward()
+    gc1, gf1 = ct.grad.clone(), f.grad.clone()
+    ct.grad = None
+    f.grad = None
+    i2, d22 = ops.binned_select_knn(ct, rs, bi, so, bb, mi, wi, sc, k, d, nb, None, None, False,
+                                    False)
+    a2 = ops.gravnet_aggregate(f, i2, d22, 10.0, [0, 1], True, so)
+    (a2 * up).sum().backward()
+    torch.testing.assert_close(gf1, f.grad, rtol=1e-5, atol=1e-6)
+    torch.testing.assert_close(gc1, ct.grad, rtol=1e-5, atol=1e-6)
