@@ -253,9 +253,16 @@ extern "C" int fg_knn_gravnet_fwd_ws(const float* sorted_coords, const int32_t* 
     if (n == 0) return 0;
     if (!feats || !agg_out) return FG_ERR_NULL;
     cudaStream_t st = (cudaStream_t)stream;
-    const bool fuse = tile_path(n_coords, n_splits, d_bin, n_bins, k, flags) && n_feats % 2 == 0 &&
-                      n_feats <= 64 && ((uintptr_t)feats % 8) == 0 && ((uintptr_t)agg_out % 8) == 0;
-    if (!fuse) {  // unfused: the search, then the aggregation (same results)
+    // In-epilogue fusion is opt-in (FG_KNN_FUSED_GN): measured on B200 (config E)
+    // the tile kernel's 16 warps/SM cannot keep enough feature gathers in flight,
+    // fused 3.2 ms vs 1.27 + 0.94 ms for the two kernels -- so by default the op
+    // runs the search and then the high-occupancy aggregation kernel.
+    const bool fuse = (flags & FG_KNN_FUSED_GN) &&
+                      tile_path(n_coords, n_splits, d_bin, n_bins, k, flags & ~FG_KNN_FUSED_GN) &&
+                      n_feats % 2 == 0 && n_feats <= 64 && ((uintptr_t)feats % 8) == 0 &&
+                      ((uintptr_t)agg_out % 8) == 0;
+    flags &= ~FG_KNN_FUSED_GN;
+    if (!fuse) {  // the search, then the aggregation (same results)
         FG_TRY(fg_knn_fwd_ws(sorted_coords, sort_order, bin_idx, bin_bounds, row_splits, dim_mins,
                              widths, n, n_coords, n_splits, d_bin, n_bins, k, nullptr, 0.0, flags,
                              out_idx, out_d2, workspace, workspace_bytes, stream));
