@@ -61,6 +61,7 @@ enum fg_status {
 #define FG_KNN_STATS 0x100       /* diagnostics: count search events (fg_knn_stats)        */
 #define FG_KNN_NO_TILE 0x200     /* diagnostics: skip the lane-per-query tile path         */
 #define FG_KNN_FUSED_GN 0x400    /* fg_knn_gravnet_fwd_ws: aggregate inside the tile epilogue */
+#define FG_KNN_FUSED_EPI 0x800   /* diagnostics: tile epilogue inside the scan kernel      */
 
 /* Reducer codes for the GravNet aggregation (G/gravnet.py:26, order = blocks). */
 #define FG_REDUCE_MEAN 0

@@ -24,6 +24,7 @@ FG_KNN_D2_F64 = 0x8
 FG_KNN_STATS = 0x100
 FG_KNN_NO_TILE = 0x200
 FG_KNN_FUSED_GN = 0x400
+FG_KNN_FUSED_EPI = 0x800
 FG_REDUCE_MEAN = 0
 FG_REDUCE_MAX = 1
 

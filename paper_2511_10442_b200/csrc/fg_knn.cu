@@ -29,7 +29,7 @@ constexpr int kStatsTotal = ST_COUNT + tile::TS_COUNT;
 bool tile_path(int32_t n_coords, int32_t n_splits, int32_t d_bin, int32_t n_bins, int32_t k,
                uint32_t flags) {
     const uint32_t off = FG_KNN_USE_DIRECTION | FG_KNN_USE_MAX_R2 | FG_KNN_EXHAUSTIVE |
-                         FG_KNN_D2_F64 | FG_KNN_NO_TILE;
+                         FG_KNN_D2_F64 | FG_KNN_NO_TILE;  // FG_KNN_FUSED_EPI / _GN: tile variants
     if (!(n_coords == d_bin && n_coords <= 4 && n_bins <= 32 && k >= 2 &&
           k - 1 <= tile::kMaxNeed && !(flags & off)))
         return false;
@@ -77,6 +77,8 @@ struct TileWs {
     int* ctr;
     int2* tiles;
     int32_t* redo;
+    int32_t* lists;  // split epilogue: n * kCap sorted positions
+    float2* meta;    //                 n * (tau, m)
     size_t bytes;
     int64_t n_blocks;
 };
@@ -97,6 +99,10 @@ TileWs tile_ws(void* base, int64_t n, int32_t n_splits, int32_t d_bin, int32_t n
     off = align_up(off + sizeof(int2) * (size_t)max_tiles, 256);
     w.redo = reinterpret_cast<int32_t*>(p + off);
     off = align_up(off + sizeof(int32_t) * (size_t)std::max<int64_t>(n, 1), 256);
+    w.lists = reinterpret_cast<int32_t*>(p + off);
+    off = align_up(off + sizeof(int32_t) * (size_t)tile::kCap * (size_t)std::max<int64_t>(n, 1), 256);
+    w.meta = reinterpret_cast<float2*>(p + off);
+    off = align_up(off + sizeof(float2) * (size_t)std::max<int64_t>(n, 1), 256);
     w.bytes = off;
     return w;
 }
@@ -210,6 +216,9 @@ extern "C" int fg_knn_fwd_ws(const float* sorted_coords, const int32_t* sort_ord
         t.redo = w.redo;
         t.out_idx = out_idx;
         t.out_d2 = reinterpret_cast<float*>(out_d2);
+        const bool split = !(flags & FG_KNN_FUSED_EPI) && !g_fused;
+        t.lists = split ? w.lists : nullptr;
+        t.meta = split ? w.meta : nullptr;
         t.stats = a.stats ? a.stats + ST_COUNT : nullptr;
         return tile::launch(t, a, d_bin, st);
     }

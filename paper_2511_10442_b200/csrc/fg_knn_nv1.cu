@@ -24,6 +24,10 @@ int launch_db(TileArgs& t, const search::KnnArgs& a, cudaStream_t st) {
     }
     k_tile_search<DB><<<(unsigned)(sms * kCtasPerSm), kWarps * 32, tile_smem_bytes(), st>>>(t);
     FG_TRY(launched(st));
+    if (t.lists) {  // split epilogue
+        k_tile_finish<DB><<<(unsigned)(sms * 8), kFinishWarps * 32, 0, st>>>(t, a.n);
+        FG_TRY(launched(st));
+    }
     // whatever the tiles could not certify: the warp-per-query kernel
     search::KnnArgs r = a;
     r.qlist = t.redo;

@@ -83,6 +83,10 @@ struct TileArgs {
     int32_t* out_idx;
     float* out_d2;
     unsigned long long* stats;
+    // split epilogue (non-null): the scan kernel writes each query's candidate
+    // list (sorted positions, kCap per query) and (tau, m); k_tile_finish sorts
+    int32_t* lists;
+    float2* meta;
     // fused GravNet aggregation of every row the tile path writes (null: off)
     const float* gn_feats;  // (n, gn_F) in original order
     float* gn_out;          // (n, gn_F * gn_n_red)
@@ -450,7 +454,8 @@ __device__ __forceinline__ void push_redo(const TileArgs& a, bool redo, int32_t 
 // exp(-scale d2) and all sums / maxima in float64, slots in order, lanes over
 // features (2 per lane, F <= 64), 4 gathers in flight -- the same arithmetic and
 // order as fg_gravnet_fwd, without re-reading the (N, k) neighbour matrix.
-__device__ __forceinline__ void fused_gravnet(const TileArgs& a, const TileWarp& W, int32_t qid) {
+template <class WS>
+__device__ __forceinline__ void fused_gravnet(const TileArgs& a, const WS& W, int32_t qid) {
     const int lane = lane_id();
     const int k = a.k, F = a.gn_F;
     const int s_begin = a.gn_incl ? 0 : 1;
@@ -528,8 +533,8 @@ __device__ __forceinline__ void fetch_query(const TileWarp& W, const TileArgs& a
     }
 }
 
-template <int DB>
-__device__ __forceinline__ bool finish_query(TileWarp& W, const TileArgs& a, int j, const QLoads& Q,
+template <int DB, class WS>
+__device__ __forceinline__ bool finish_query(WS& W, const TileArgs& a, int j, const QLoads& Q,
                                              const float4 q, int32_t p, float tau, int32_t qid_l,
                                              int need) {
     const float qa[4] = {q.x, q.y, q.z, q.w};
@@ -622,10 +627,21 @@ __device__ __forceinline__ bool finish_query(TileWarp& W, const TileArgs& a, int
             int r = b0;
             bool tie = false;
             if (live) {
-                for (int i = b0; i < b1; ++i) {
-                    const float ki = W.skey[i];
-                    r += (ki < kk || (ki == kk && i < sl)) ? 1 : 0;
-                    tie |= ki == kk && i != sl;
+                if (b1 - b0 <= 3) {  // the common case: unrolled, no loop
+#pragma unroll
+                    for (int u = 0; u < 3; ++u) {
+                        const int i = b0 + u;
+                        const float ki = W.skey[min(i, kCap - 1)];
+                        const bool mate = i < b1 && i != sl;
+                        r += (mate && (ki < kk || (ki == kk && i < sl))) ? 1 : 0;
+                        tie |= mate && ki == kk;
+                    }
+                } else {
+                    for (int i = b0; i < b1; ++i) {
+                        const float ki = W.skey[i];
+                        r += (ki < kk || (ki == kk && i < sl)) ? 1 : 0;
+                        tie |= ki == kk && i != sl;
+                    }
                 }
             }
             if (live) {
@@ -711,6 +727,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) k_tile_search(const _
                 const int32_t L = __shfl_sync(FG_FULL_MASK, rL, r);
                 for (int i0 = 0; i0 < L; i0 += 32) {
                     push_redo(a, i0 + lane < L, S + i0 + lane);
+                    if (a.meta && i0 + lane < L) a.meta[S + i0 + lane] = make_float2(0.f, -1.f);
                     st_redo += (i0 + lane < L) ? 1 : 0;
                 }
             }
@@ -853,6 +870,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) k_tile_search(const _
         if (bad) {
             ++st_fail;
             push_redo(a, active, p);
+            if (a.meta && active) a.meta[p] = make_float2(0.f, -1.f);
             st_redo += active ? 1 : 0;
             __syncwarp();
             continue;
@@ -907,6 +925,28 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) k_tile_search(const _
         __syncwarp();
         continue;
 #endif
+        if (a.lists) {  // split epilogue: hand the lists to k_tile_finish
+            if (active && !overflow) {
+                const uint16_t* L = &W.code[lane * kStride];
+                int4* dst = reinterpret_cast<int4*>(a.lists + (int64_t)p * kCap);
+                for (int e = 0; e < m_l; e += 4) {
+                    int32_t v4[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const uint16_t cd = L[min(e + u, m_l - 1)];
+                        v4[u] = W.spS[cd >> 7] + (cd & 127);
+                    }
+                    dst[e >> 2] = make_int4(v4[0], v4[1], v4[2], v4[3]);
+                }
+                a.meta[p] = make_float2(tau, (float)m_l);
+            }
+            const bool redo = active && overflow;
+            if (redo) a.meta[p] = make_float2(0.f, -1.f);
+            push_redo(a, redo, p);
+            st_redo += redo ? 1 : 0;
+            __syncwarp();
+            continue;
+        }
         const unsigned todo = __ballot_sync(FG_FULL_MASK, active && !overflow);
         bool ok = false;  // this lane's query got its row
         const int32_t qid_l = active ? a.sid[p] : 0;
@@ -935,6 +975,59 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) k_tile_search(const _
             atomicAdd(&a.stats[TS_EXPANDED], st_exp);
         }
     }
+}
+
+// ---------------------------------------------------------------- split epilogue
+struct FinishWarp {
+    float skey[kCap];
+    int32_t sid[kCap];
+    alignas(16) float okey[kCap + 4];
+    alignas(16) int32_t oid[kCap + 4];
+    alignas(16) uint32_t bcnt[kBkt + 4];
+};
+constexpr int kFinishWarps = 8;
+#ifndef FG_FINISH_MINB
+#define FG_FINISH_MINB 4
+#endif
+
+// Warp per query in sorted order (neighbouring warps share candidates in L1/L2),
+// the lists written by k_tile_search; the same finish_query as the fused path.
+template <int DB>
+__global__ void __launch_bounds__(kFinishWarps * 32, FG_FINISH_MINB) k_tile_finish(const __grid_constant__ TileArgs a,
+                                                                   int64_t n) {
+    __shared__ FinishWarp fw[kFinishWarps];
+    FinishWarp& W = fw[threadIdx.x >> 5];
+    const int lane = lane_id();
+    const int need = a.k - 1;
+    unsigned long long st_redo = 0;
+    for (int64_t p = blockIdx.x * (int64_t)kFinishWarps + (threadIdx.x >> 5); p < n;
+         p += (int64_t)gridDim.x * kFinishWarps) {
+        const float2 mt = a.meta[p];
+        const int m = (int)mt.y;
+        if (m < 0) continue;  // already on the redo list
+        QLoads Q;
+        Q.m = m;
+        const int32_t* lp = a.lists + p * kCap;
+#pragma unroll
+        for (int t = 0; t < kRounds; ++t) {
+            const int e = lane + 32 * t;
+            Q.cpos[t] = -1;
+            if (32 * t < m && e < m) {
+                Q.cpos[t] = lp[e];
+                Q.c[t] = a.sc[Q.cpos[t]];
+                Q.id[t] = a.sid[Q.cpos[t]];
+            }
+        }
+        const float4 q = a.sc[p];
+        const int32_t qid = a.sid[p];
+        const bool ok = finish_query<DB>(W, a, 0, Q, q, (int32_t)p, mt.x, qid, need);
+        if (!ok && lane == 0) {
+            a.redo[atomicAdd(&a.ctr[2], 1)] = (int32_t)p;
+            ++st_redo;
+        }
+        __syncwarp();
+    }
+    if (a.stats && lane == 0 && st_redo) atomicAdd(&a.stats[TS_REDO], st_redo);
 }
 
 }  // namespace tile
