@@ -14,15 +14,24 @@ int launch_db(TileArgs& t, const search::KnnArgs& a, cudaStream_t st) {
     FG_CUDA(cudaMemsetAsync(t.ctr, 0, 4 * sizeof(int), st));
     k_tiles<DB><<<(unsigned)ceil_div(t.n_blocks, 4), 128, 0, st>>>(t);
     FG_TRY(launched(st));
-    static int sms = 0;  // per template instance: also sets the smem opt-in once
+    static int sms = 0;  // per template instance: also sets the smem opt-ins once
     if (!sms) {
         int dev = 0;
         FG_CUDA(cudaGetDevice(&dev));
-        FG_CUDA(cudaFuncSetAttribute(k_tile_search<DB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)tile_smem_bytes()));
+        FG_CUDA(cudaFuncSetAttribute(k_tile_search<DB, false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)tile_smem_bytes<false>()));
+        FG_CUDA(cudaFuncSetAttribute(k_tile_search<DB, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)tile_smem_bytes<true>()));
         FG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     }
-    k_tile_search<DB><<<(unsigned)(sms * kCtasPerSm), kWarps * 32, tile_smem_bytes(), st>>>(t);
+    if (t.lists)
+        k_tile_search<DB, true><<<(unsigned)(sms * kScanCtasPerSm), kWarps * 32,
+                                  tile_smem_bytes<true>(), st>>>(t);
+    else
+        k_tile_search<DB, false><<<(unsigned)(sms * kCtasPerSm), kWarps * 32,
+                                   tile_smem_bytes<false>(), st>>>(t);
     FG_TRY(launched(st));
     if (t.lists) {  // split epilogue
         k_tile_finish<DB><<<(unsigned)(sms * 8), kFinishWarps * 32, 0, st>>>(t, a.n);

@@ -40,6 +40,8 @@
 //   oversize tile, ties) is appended to a redo list that the warp-per-query
 //   kernel finishes in a second launch -- same canonical answer either way.
 #pragma once
+#include <type_traits>
+
 #include "fg_knn_impl.cuh"
 
 namespace fg {
@@ -95,23 +97,38 @@ struct TileArgs {
     double gn_scale;
 };
 
-struct TileWarp {
+// Per-warp shared memory of the scan.
+struct ScanWarp {
     uint16_t code[32 * kStride];          // [lane][slot] per-lane candidate lists
-    float skey[kCap];                     // epilogue staging of one query: keys
-    int32_t sid[kCap];                    //   and original ids, in bucket order
-    alignas(16) float okey[kCap + 4];     //   final row: slot 0 = self, then by key
-    alignas(16) int32_t oid[kCap + 4];
-    alignas(16) uint32_t bcnt[kBkt + 4];  //   bucket counts -> starts
     int32_t spS[kMaxSpans];               // span start (sorted position)
     uint16_t spE[kMaxSpans + 1];          // span flattened start (exclusive prefix)
     alignas(16) float sx[4][32];          // chunk coordinates, SoA (centred in expanded mode)
     alignas(16) float sn[32];             // expanded mode: |c - centre|^2
     alignas(16) uint32_t scode[32];       // chunk codes
 };
+// ... plus the epilogue staging when the scan kernel finishes its own queries
+// (FG_KNN_FUSED_EPI, fused GravNet).
+struct TileWarp : ScanWarp {
+    float skey[kCap];                     // epilogue staging of one query: keys
+    int32_t sid[kCap];                    //   and original ids, in bucket order
+    alignas(16) float okey[kCap + 4];     //   final row: slot 0 = self, then by key
+    alignas(16) int32_t oid[kCap + 4];
+    alignas(16) uint32_t bcnt[kBkt + 4];  //   bucket counts -> starts
+};
 
-__host__ __device__ constexpr size_t tile_smem_bytes() { return sizeof(TileWarp) * kWarps; }
-static_assert(tile_smem_bytes() * kCtasPerSm + 1024 * kCtasPerSm <= 233472,
+#ifndef FG_SCAN_CTAS
+#define FG_SCAN_CTAS 5
+#endif
+constexpr int kScanCtasPerSm = FG_SCAN_CTAS;  // the split-epilogue scan kernel
+
+template <bool SPLIT>
+__host__ __device__ constexpr size_t tile_smem_bytes() {
+    return (SPLIT ? sizeof(ScanWarp) : sizeof(TileWarp)) * kWarps;
+}
+static_assert(tile_smem_bytes<false>() * kCtasPerSm + 1024 * kCtasPerSm <= 233472,
               "k_tile_search: CTAs per SM do not fit in shared memory");
+static_assert(tile_smem_bytes<true>() * kScanCtasPerSm + 1024 * kScanCtasPerSm <= 233472,
+              "k_tile_search (split): CTAs per SM do not fit in shared memory");
 
 // Lead block `b` of a split -> origin cells (last lead dim fastest).
 template <int NL>
@@ -319,7 +336,7 @@ __device__ __forceinline__ unsigned long long pack2(float x) {
 // Stream the tile's candidates in 32-candidate chunks (coalesced loads into
 // shared memory, then broadcast) and append each lane's passing codes.
 template <bool EXP>
-__device__ __forceinline__ void scan_tile(TileWarp& W, const float4* __restrict__ sc, int T, int nsp,
+__device__ __forceinline__ void scan_tile(ScanWarp& W, const float4* __restrict__ sc, int T, int nsp,
                                           const QP& qv, const QX& qx, const float4 cen, float tau,
                                           uint32_t& ptr, bool& overflow, uint32_t llim) {
     const int lane = lane_id();
@@ -515,7 +532,7 @@ struct QLoads {
     int m;
 };
 
-__device__ __forceinline__ void fetch_query(const TileWarp& W, const TileArgs& a, int j, int m_l,
+__device__ __forceinline__ void fetch_query(const ScanWarp& W, const TileArgs& a, int j, int m_l,
                                             QLoads& Q) {
     const int lane = lane_id();
     Q.m = __shfl_sync(FG_FULL_MASK, m_l, j);
@@ -677,11 +694,13 @@ __device__ __forceinline__ bool finish_query(WS& W, const TileArgs& a, int j, co
 }
 
 // ---------------------------------------------------------------- search
-template <int DB>
-__global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) k_tile_search(const __grid_constant__ TileArgs a) {
+template <int DB, bool SPLIT>
+__global__ void __launch_bounds__(kWarps * 32, SPLIT ? kScanCtasPerSm : kCtasPerSm)
+    k_tile_search(const __grid_constant__ TileArgs a) {
     constexpr int NL = DB - 1;
+    using WT = typename std::conditional<SPLIT, ScanWarp, TileWarp>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    TileWarp& W = reinterpret_cast<TileWarp*>(smem_raw)[threadIdx.x >> 5];
+    WT& W = reinterpret_cast<WT*>(smem_raw)[threadIdx.x >> 5];
     const int lane = lane_id();
     const int nb = a.nb;
     const int need = a.k - 1;
@@ -925,7 +944,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) k_tile_search(const _
         __syncwarp();
         continue;
 #endif
-        if (a.lists) {  // split epilogue: hand the lists to k_tile_finish
+        if constexpr (SPLIT) {  // split epilogue: hand the lists to k_tile_finish
             if (active && !overflow) {
                 const uint16_t* L = &W.code[lane * kStride];
                 int4* dst = reinterpret_cast<int4*>(a.lists + (int64_t)p * kCap);
@@ -947,23 +966,25 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) k_tile_search(const _
             __syncwarp();
             continue;
         }
-        const unsigned todo = __ballot_sync(FG_FULL_MASK, active && !overflow);
-        bool ok = false;  // this lane's query got its row
-        const int32_t qid_l = active ? a.sid[p] : 0;
-        QLoads cur, nxt;
-        if (todo) fetch_query(W, a, __ffs(todo) - 1, m_l, cur);
-        for (unsigned mask = todo; mask;) {
-            const int j = __ffs(mask) - 1;
-            mask &= mask - 1;
-            if (mask) fetch_query(W, a, __ffs(mask) - 1, m_l, nxt);  // next query's gathers
-            const bool okj = finish_query<DB>(W, a, j, cur, q, p, tau, qid_l, need);
-            if (lane == j) ok = okj;
-            cur = nxt;
+        if constexpr (!SPLIT) {
+            const unsigned todo = __ballot_sync(FG_FULL_MASK, active && !overflow);
+            bool ok = false;  // this lane's query got its row
+            const int32_t qid_l = active ? a.sid[p] : 0;
+            QLoads cur, nxt;
+            if (todo) fetch_query(W, a, __ffs(todo) - 1, m_l, cur);
+            for (unsigned mask = todo; mask;) {
+                const int j = __ffs(mask) - 1;
+                mask &= mask - 1;
+                if (mask) fetch_query(W, a, __ffs(mask) - 1, m_l, nxt);  // next query's gathers
+                const bool okj = finish_query<DB>(W, a, j, cur, q, p, tau, qid_l, need);
+                if (lane == j) ok = okj;
+                cur = nxt;
+            }
+            const bool redo = active && !ok;
+            push_redo(a, redo, p);
+            st_redo += redo ? 1 : 0;
+            __syncwarp();
         }
-        const bool redo = active && !ok;
-        push_redo(a, redo, p);
-        st_redo += redo ? 1 : 0;
-        __syncwarp();
     }
     if (a.stats) {
         st_redo = __reduce_add_sync(FG_FULL_MASK, (unsigned)st_redo);
