@@ -98,8 +98,11 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_knn_bwd(const float* __restr
 // flight at once -- the coordinate gathers, then the returning fp32x4 atomics,
 // then the TwoSum corrections -- so the L2 round trips of 2*RPW chains overlap
 // (the warp-per-row kernel above waits for each one).  Same arithmetic.
+#ifndef FG_BWD_MINB
+#define FG_BWD_MINB 4
+#endif
 template <int RPW, int SR>
-__global__ void __launch_bounds__(kRowWarps * 32) k_knn_bwd_pipe(
+__global__ void __launch_bounds__(kRowWarps * 32, FG_BWD_MINB) k_knn_bwd_pipe(
     const float* __restrict__ coords, int64_t n, int n_c, const int32_t* __restrict__ idx, int k,
     const float* __restrict__ gd2, const int32_t* __restrict__ order, float4* __restrict__ hi,
     float4* __restrict__ lo) {
