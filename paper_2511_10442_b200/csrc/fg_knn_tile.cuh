@@ -404,13 +404,21 @@ __device__ __forceinline__ void scan_tile(ScanWarp& W, const float4* __restrict_
                 }
             }
         } else {
-            // direct form (the ~10% of tiles the expanded bound rejects): rolled, small code
-#pragma unroll 1
+            // direct form: 4 floats per candidate from shared memory (the scan is
+            // bound by the shared-memory pipe; the expanded form reads 5)
+            uint32_t cd[32];
+#pragma unroll
             for (int j = 0; j < 8; ++j) {
-                G4 gq;
-                load_g4(gq, sx_addr, 4 * j);
-                const uint4 cv = reinterpret_cast<const uint4*>(W.scode)[j];
-                eval_g4(gq, qv, tau, ptr, cv.x, cv.y, cv.z, cv.w);
+                const uint4 v = reinterpret_cast<const uint4*>(W.scode)[j];
+                cd[4 * j] = v.x; cd[4 * j + 1] = v.y; cd[4 * j + 2] = v.z; cd[4 * j + 3] = v.w;
+            }
+            G4 gb[2];
+            load_g4(gb[0], sx_addr, 0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (j + 1 < 8) load_g4(gb[(j + 1) & 1], sx_addr, 4 * (j + 1));
+                eval_g4(gb[j & 1], qv, tau, ptr, cd[4 * j], cd[4 * j + 1], cd[4 * j + 2],
+                        cd[4 * j + 3]);
                 if (j == 3 && ptr > llim) {
                     overflow = true;
                     ptr = llim;
@@ -922,7 +930,10 @@ __global__ void __launch_bounds__(kWarps * 32, SPLIT ? kScanCtasPerSm : kCtasPer
         const float rq = warp_max_f(active ? sqrtf(sq) : 0.0f);
         const float tau_min = warp_min_f(active ? tau : kInf);
         const float rsum = (rq + sqrtf(rc2)) * 1.01f;
-        const bool expanded = rsum * rsum <= 32.0f * tau_min;
+#ifndef FG_TILE_EXPANDED
+#define FG_TILE_EXPANDED 0
+#endif
+        const bool expanded = FG_TILE_EXPANDED && rsum * rsum <= 32.0f * tau_min;
         QX qx;
         qx.sq = pack2(sq);
         qx.m2q[0] = pack2(-2.0f * qs.x);
