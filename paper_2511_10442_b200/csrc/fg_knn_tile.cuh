@@ -104,7 +104,7 @@ struct ScanWarp {
     uint16_t spE[kMaxSpans + 1];          // span flattened start (exclusive prefix)
     alignas(16) float sx[4][32];          // chunk coordinates, SoA (centred in expanded mode)
     alignas(16) float sn[32];             // expanded mode: |c - centre|^2
-    alignas(16) uint32_t scode[32];       // chunk codes
+    alignas(16) uint16_t scode[32];       // chunk codes
 };
 // ... plus the epilogue staging when the scan kernel finishes its own queries
 // (FG_KNN_FUSED_EPI, fused GravNet).
@@ -381,15 +381,20 @@ __device__ __forceinline__ void scan_tile(ScanWarp& W, const float4* __restrict_
         W.sx[2][lane] = c.z;
         W.sx[3][lane] = c.w;
         if (EXP) W.sn[lane] = nn;
-        W.scode[lane] = code;
+        W.scode[lane] = (uint16_t)code;
         __syncwarp();
         // software pipeline: the next group's loads precede this group's stores
         if (EXP) {
             uint32_t cd[32];  // the chunk's codes (uniform), in registers
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < 4; ++j) {
                 const uint4 v = reinterpret_cast<const uint4*>(W.scode)[j];
-                cd[4 * j] = v.x; cd[4 * j + 1] = v.y; cd[4 * j + 2] = v.z; cd[4 * j + 3] = v.w;
+                const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    cd[8 * j + 2 * h] = w4[h];
+                    cd[8 * j + 2 * h + 1] = w4[h] >> 16;
+                }
             }
             G4X gb[2];
             load_g4x(gb[0], sx_addr, 0);
@@ -405,12 +410,18 @@ __device__ __forceinline__ void scan_tile(ScanWarp& W, const float4* __restrict_
             }
         } else {
             // direct form: 4 floats per candidate from shared memory (the scan is
-            // bound by the shared-memory pipe; the expanded form reads 5)
+            // bound by the shared-memory pipe; the expanded form reads 5); the
+            // 16-bit codes come in 4 vector loads, odd ones shifted down
             uint32_t cd[32];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < 4; ++j) {
                 const uint4 v = reinterpret_cast<const uint4*>(W.scode)[j];
-                cd[4 * j] = v.x; cd[4 * j + 1] = v.y; cd[4 * j + 2] = v.z; cd[4 * j + 3] = v.w;
+                const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    cd[8 * j + 2 * h] = w4[h];  // st.shared.u16 keeps the low half
+                    cd[8 * j + 2 * h + 1] = w4[h] >> 16;
+                }
             }
             G4 gb[2];
             load_g4(gb[0], sx_addr, 0);
