@@ -67,7 +67,7 @@ constexpr float kSlackCells = 1e-4f;
 constexpr float kInf = __builtin_huge_valf();
 constexpr int kMaxNeed = 40;       // host eligibility: k - 1 <= kMaxNeed
 
-enum { TS_TILES, TS_CAND, TS_REDO, TS_TILE_FAIL, TS_EXPANDED, TS_COUNT };
+enum { TS_TILES, TS_CAND, TS_REDO, TS_TILE_FAIL, TS_EXPANDED, TS_EVAL, TS_COUNT };
 
 struct TileArgs {
     const float4* sc;
@@ -102,9 +102,9 @@ struct ScanWarp {
     uint16_t code[32 * kStride];          // [lane][slot] per-lane candidate lists
     int32_t spS[kMaxSpans];               // span start (sorted position)
     uint16_t spE[kMaxSpans + 1];          // span flattened start (exclusive prefix)
-    alignas(16) float sx[4][32];          // chunk coordinates, SoA (centred in expanded mode)
+    alignas(16) float sx[4][64];          // candidate ring (2 chunks), SoA (centred when expanded)
     alignas(16) float sn[32];             // expanded mode: |c - centre|^2
-    alignas(16) uint16_t scode[32];       // chunk codes
+    alignas(16) uint16_t scode[64];       // ring codes
 };
 // ... plus the epilogue staging when the scan kernel finishes its own queries
 // (FG_KNN_FUSED_EPI, fused GravNet).
@@ -267,7 +267,7 @@ __device__ __forceinline__ void load_g4(G4& g, uint32_t sx_addr, int j) {
     for (int d = 0; d < 4; ++d)
         asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];"
                      : "=l"(g.x[d][0]), "=l"(g.x[d][1])
-                     : "r"(sx_addr + d * 128 + j * 4));
+                     : "r"(sx_addr + d * 256 + j * 4));
 }
 
 // d2 of 4 candidates against the lane's query (packed over candidate pairs),
@@ -308,10 +308,10 @@ __device__ __forceinline__ void load_g4x(G4X& g, uint32_t sx_addr, int j) {
     for (int d = 0; d < 4; ++d)
         asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];"
                      : "=l"(g.x[d][0]), "=l"(g.x[d][1])
-                     : "r"(sx_addr + d * 128 + j * 4));
+                     : "r"(sx_addr + d * 256 + j * 4));
     asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];"
                  : "=l"(g.n[0]), "=l"(g.n[1])
-                 : "r"(sx_addr + 4 * 128 + j * 4));
+                 : "r"(sx_addr + 4 * 256 + j * 4));
 }
 __device__ __forceinline__ void eval_g4x(const G4X& g, const QX& q, float tau_x, uint32_t& ptr,
                                          uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3) {
@@ -441,6 +441,105 @@ __device__ __forceinline__ void scan_tile(ScanWarp& W, const float4* __restrict_
             ptr = llim;
         }
         __syncwarp();
+    }
+}
+
+// Direct-form scan with a per-candidate filter: a candidate farther than
+// sqrt(tau_max) from the tile's query bounding box cannot enter any lane's list
+// (about half of the region's candidates at north_star: the region is built
+// at cell granularity).  Fetched chunks are compacted into a 64-entry ring and
+// evaluated 32 at a time, so the broadcast loop only sees useful candidates.
+__device__ __forceinline__ void scan_tile_filtered(ScanWarp& W, const float4* __restrict__ sc, int T,
+                                                   int nsp, const QP& qv, float tau,
+                                                   const float4 blo, const float4 bhi, float thr,
+                                                   uint32_t& ptr, bool& overflow, uint32_t llim,
+                                                   unsigned long long& n_eval) {
+    const int lane = lane_id();
+    const uint32_t sx_addr = (uint32_t)__cvta_generic_to_shared(&W.sx[0][0]);
+    int s0 = 0;
+    auto fetch = [&](int f0, float4& c, uint32_t& code, bool& live) {
+        const int f = f0 + lane;
+        const int si = s0 + lane;
+        const int st = si < nsp ? W.spE[si] : 0x7fffffff;
+        const unsigned starts = __reduce_or_sync(
+            FG_FULL_MASK, (lane > 0 && st > f0 && st < f0 + 32) ? 1u << (st - f0) : 0u);
+        const int g = s0 + __popc(starts & ((2u << lane) - 1u));
+        live = f < T;
+        code = 0;
+        if (live) {
+            const int off = f - W.spE[g];
+            c = sc[W.spS[g] + off];
+            code = (uint32_t)((g << 7) | off);
+        }
+        s0 = __shfl_sync(FG_FULL_MASK, g, 31);
+        if (s0 + 1 < nsp && W.spE[s0 + 1] == f0 + 32) ++s0;
+    };
+    float4 cn = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t coden = 0;
+    bool liven = false;
+    int fpos = 0;
+    if (T > 0) fetch(0, cn, coden, liven);
+    int head = 0, filled = 0;
+    for (;;) {
+        while (filled < 32 && fpos < T) {  // fill the ring with useful candidates
+            const float4 c = cn;
+            const uint32_t code = coden;
+            const bool live = liven;
+            fpos += 32;
+            if (fpos < T) fetch(fpos, cn, coden, liven);  // next raw chunk in flight
+            float g = fmaxf(fmaxf(blo.x - c.x, c.x - bhi.x), 0.0f);
+            float dd = g * g;
+            g = fmaxf(fmaxf(blo.y - c.y, c.y - bhi.y), 0.0f);
+            dd = fmaf(g, g, dd);
+            g = fmaxf(fmaxf(blo.z - c.z, c.z - bhi.z), 0.0f);
+            dd = fmaf(g, g, dd);
+            g = fmaxf(fmaxf(blo.w - c.w, c.w - bhi.w), 0.0f);
+            dd = fmaf(g, g, dd);
+            const bool useful = live && dd <= thr;
+            const unsigned bal = __ballot_sync(FG_FULL_MASK, useful);
+            if (useful) {
+                const int slot = (head + filled + __popc(bal & lanemask_lt())) & 63;
+                W.sx[0][slot] = c.x;
+                W.sx[1][slot] = c.y;
+                W.sx[2][slot] = c.z;
+                W.sx[3][slot] = c.w;
+                W.scode[slot] = (uint16_t)code;
+            }
+            filled += __popc(bal);
+        }
+        if (filled == 0) break;
+        if (filled < 32 && lane >= filled) {  // last round: pad with far-away sentinels
+            const int slot = (head + lane) & 63;
+            W.sx[0][slot] = kInf; W.sx[1][slot] = kInf; W.sx[2][slot] = kInf; W.sx[3][slot] = kInf;
+        }
+        __syncwarp();
+        n_eval += 32;
+        const uint32_t base = sx_addr + head * 4;
+        uint32_t cd[32];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint4 v = reinterpret_cast<const uint4*>(&W.scode[head])[j];
+            const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                cd[8 * j + 2 * h] = w4[h];  // st.shared.u16 keeps the low half
+                cd[8 * j + 2 * h + 1] = w4[h] >> 16;
+            }
+        }
+        G4 gb[2];
+        load_g4(gb[0], base, 0);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (j + 1 < 8) load_g4(gb[(j + 1) & 1], base, 4 * (j + 1));
+            eval_g4(gb[j & 1], qv, tau, ptr, cd[4 * j], cd[4 * j + 1], cd[4 * j + 2], cd[4 * j + 3]);
+            if ((j & 3) == 3 && ptr > llim) {  // clamp every 16 candidates (kSlack)
+                overflow = true;
+                ptr = llim;
+            }
+        }
+        __syncwarp();
+        head ^= 32;
+        filled = max(filled - 32, 0);
     }
 }
 
@@ -724,7 +823,7 @@ __global__ void __launch_bounds__(kWarps * 32, SPLIT ? kScanCtasPerSm : kCtasPer
     const int nb = a.nb;
     const int need = a.k - 1;
     const int n_tiles = a.ctr[0];
-    unsigned long long st_cand = 0, st_tiles = 0, st_redo = 0, st_fail = 0, st_exp = 0;
+    unsigned long long st_cand = 0, st_tiles = 0, st_redo = 0, st_fail = 0, st_exp = 0, st_eval = 0;
 
     for (;;) {
         int t = 0;
@@ -953,10 +1052,20 @@ __global__ void __launch_bounds__(kWarps * 32, SPLIT ? kScanCtasPerSm : kCtasPer
         qx.m2q[3] = pack2(-2.0f * qs.w);
         qx.tau_x = tau - sq;
         st_exp += expanded ? 1 : 0;
-        if (expanded)
+        if (expanded) {
             scan_tile<true>(W, a.sc, T, nsp, qv, qx, cen, tau, ptr, overflow, llim);
-        else
-            scan_tile<false>(W, a.sc, T, nsp, qv, qx, cen, tau, ptr, overflow, llim);
+        } else {
+            float bl[4] = {0.f, 0.f, 0.f, 0.f}, bh[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int i = 0; i < DB; ++i) {  // the queries' physical bounding box
+                bl[i] = warp_min_f(active ? qa[i] : kInf);
+                bh[i] = warp_max_f(active ? qa[i] : -kInf);
+            }
+            const float thr = tau_max * kMargin + 1e-30f;
+            scan_tile_filtered(W, a.sc, T, nsp, qv, tau, make_float4(bl[0], bl[1], bl[2], bl[3]),
+                               make_float4(bh[0], bh[1], bh[2], bh[3]), thr, ptr, overflow, llim,
+                               st_eval);
+        }
         asm volatile("" ::: "memory");  // list stores (inline asm) before the epilogue reads
 
         // ---- epilogue: the warp finishes the lanes' queries one at a time
@@ -1016,6 +1125,7 @@ __global__ void __launch_bounds__(kWarps * 32, SPLIT ? kScanCtasPerSm : kCtasPer
             atomicAdd(&a.stats[TS_REDO], st_redo);
             atomicAdd(&a.stats[TS_TILE_FAIL], st_fail);
             atomicAdd(&a.stats[TS_EXPANDED], st_exp);
+            atomicAdd(&a.stats[TS_EVAL], st_eval);
         }
     }
 }

@@ -51,4 +51,5 @@ for name, c, off, k in cases:
     q = max(s1["tiles"], 1)
     print(f"{name}: exact={same} bad_rows={bad} warp_ms={t0:.3f} tile_ms={t1:.3f} "
           f"tiles={s1['tiles']} cand/tile={s1['tile_candidates']/q:.0f} redo={s1['tile_redo']} "
-          f"({100*s1['tile_redo']/len(c):.3f}%) tile_fail={s1['tile_fail']} expanded={s1['tile_expanded']}", flush=True)
+          f"({100*s1['tile_redo']/len(c):.3f}%) tile_fail={s1['tile_fail']} expanded={s1['tile_expanded']} "
+          f"eval/tile={s1['tile_evaluated']/q:.0f}", flush=True)
