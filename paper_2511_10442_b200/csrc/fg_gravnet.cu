@@ -38,6 +38,15 @@ namespace fg {
 namespace gravnet {
 
 constexpr int kRowWarps = 8;
+#ifndef FG_GN_ROWS_MINB
+#define FG_GN_ROWS_MINB 5
+#endif
+#ifndef FG_GN_COLS_MINB
+#define FG_GN_COLS_MINB 6
+#endif
+#ifndef FG_GN_FWD_MINB
+#define FG_GN_FWD_MINB 4
+#endif
 constexpr int U = 8;  // gathers in flight per warp
 
 struct GnArgs {
@@ -194,7 +203,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_gn_fwd(const GnArgs g, int f
 #endif
 
 template <int UP>
-__global__ void __launch_bounds__(kRowWarps * 32) k_gn_fwd_pairs(const GnArgs g, float* __restrict__ out) {
+__global__ void __launch_bounds__(kRowWarps * 32, FG_GN_FWD_MINB) k_gn_fwd_pairs(const GnArgs g, float* __restrict__ out) {
     const int lane = lane_id();
     const int64_t p = blockIdx.x * (int64_t)kRowWarps + (threadIdx.x >> 5);
     if (p >= g.n) return;
@@ -459,7 +468,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_gn_rows(const GnArgs g, cons
 // and their feature gradient goes to the arg-max neighbour as before.  Same
 // arithmetic as k_gn_rows (which gathers twice: arg-max first, then the dots).
 template <int VW>
-__global__ void __launch_bounds__(kRowWarps * 32) k_gn_rows1(const GnArgs g, const GnBwd bw, int f0,
+__global__ void __launch_bounds__(kRowWarps * 32, FG_GN_ROWS_MINB) k_gn_rows1(const GnArgs g, const GnBwd bw, int f0,
                                                            int last_chunk) {
     constexpr int UR = 4;  // gathers in flight (fewer registers, more warps)
     __shared__ double extra_s[kRowWarps][64];
@@ -596,7 +605,7 @@ __global__ void k_gn_fill(const GnArgs g, const GnBwd bw) {
 #define FG_GN_COLS_U 2
 #endif
 template <int VW>
-__global__ void __launch_bounds__(kRowWarps * 32) k_gn_cols(const GnArgs g, const GnBwd bw, int f0) {
+__global__ void __launch_bounds__(kRowWarps * 32, FG_GN_COLS_MINB) k_gn_cols(const GnArgs g, const GnBwd bw, int f0) {
     constexpr int UC = FG_GN_COLS_U;
     const int lane = lane_id();
     const int64_t p = blockIdx.x * (int64_t)kRowWarps + (threadIdx.x >> 5);
