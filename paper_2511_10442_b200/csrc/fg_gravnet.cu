@@ -38,15 +38,6 @@ namespace fg {
 namespace gravnet {
 
 constexpr int kRowWarps = 8;
-#ifndef FG_GN_ROWS_MINB
-#define FG_GN_ROWS_MINB 5
-#endif
-#ifndef FG_GN_COLS_MINB
-#define FG_GN_COLS_MINB 6
-#endif
-#ifndef FG_GN_FWD_MINB
-#define FG_GN_FWD_MINB 4
-#endif
 constexpr int U = 8;  // gathers in flight per warp
 
 struct GnArgs {
@@ -69,8 +60,11 @@ struct GnArgs {
 };
 
 __device__ __forceinline__ int64_t row_of(const GnArgs& g, int64_t p) {
-    if (g.plist) return (int64_t)g.psid[g.plist[p]];
     return g.order ? (int64_t)g.order[p] : p;
+}
+__device__ __forceinline__ int64_t row_of_list(const GnArgs& g, int64_t p) {
+    if (g.plist) return (int64_t)g.psid[g.plist[p]];
+    return row_of(g, p);
 }
 
 __device__ __forceinline__ bool is_max(const GnArgs& g, int b) { return (g.max_bits >> b) & 1u; }
@@ -143,7 +137,7 @@ __device__ __forceinline__ void gather(const GnArgs& g, const Window& wd, int j0
 template <int VW, int UF>
 __device__ __forceinline__ void gn_fwd_row(const GnArgs& g, int f0, float* __restrict__ out, int64_t p) {
     const int lane = lane_id();
-    const int64_t v = row_of(g, p);
+    const int64_t v = row_of_list(g, p);
     const int k = g.k, F = g.F, W = F * g.n_red;
     const int fl = f0 + lane * VW;
     const bool lane_on = fl < F;
@@ -203,7 +197,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_gn_fwd(const GnArgs g, int f
 #endif
 
 template <int UP>
-__global__ void __launch_bounds__(kRowWarps * 32, FG_GN_FWD_MINB) k_gn_fwd_pairs(const GnArgs g, float* __restrict__ out) {
+__global__ void __launch_bounds__(kRowWarps * 32) k_gn_fwd_pairs(const GnArgs g, float* __restrict__ out) {
     const int lane = lane_id();
     const int64_t p = blockIdx.x * (int64_t)kRowWarps + (threadIdx.x >> 5);
     if (p >= g.n) return;
@@ -468,7 +462,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_gn_rows(const GnArgs g, cons
 // and their feature gradient goes to the arg-max neighbour as before.  Same
 // arithmetic as k_gn_rows (which gathers twice: arg-max first, then the dots).
 template <int VW>
-__global__ void __launch_bounds__(kRowWarps * 32, FG_GN_ROWS_MINB) k_gn_rows1(const GnArgs g, const GnBwd bw, int f0,
+__global__ void __launch_bounds__(kRowWarps * 32) k_gn_rows1(const GnArgs g, const GnBwd bw, int f0,
                                                            int last_chunk) {
     constexpr int UR = 4;  // gathers in flight (fewer registers, more warps)
     __shared__ double extra_s[kRowWarps][64];
@@ -605,7 +599,7 @@ __global__ void k_gn_fill(const GnArgs g, const GnBwd bw) {
 #define FG_GN_COLS_U 2
 #endif
 template <int VW>
-__global__ void __launch_bounds__(kRowWarps * 32, FG_GN_COLS_MINB) k_gn_cols(const GnArgs g, const GnBwd bw, int f0) {
+__global__ void __launch_bounds__(kRowWarps * 32) k_gn_cols(const GnArgs g, const GnBwd bw, int f0) {
     constexpr int UC = FG_GN_COLS_U;
     const int lane = lane_id();
     const int64_t p = blockIdx.x * (int64_t)kRowWarps + (threadIdx.x >> 5);
