@@ -61,7 +61,7 @@ def load_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-SEARCH_KERNELS = ("k_tiles", "k_tile_search", "k_knn_fwd")
+SEARCH_KERNELS = ("k_tiles", "k_tile_search", "k_tile_finish", "k_knn_fwd")
 
 
 def load_traffic(config):
@@ -465,9 +465,13 @@ def main():
                    "precision": "fp32 distance filter, float64 exact epilogue / gradient sums"},
         "breakdown_ms": phase,
         "roofline": {"bound": "hbm",
-                     "kernel": ("knn_gravnet (k_tiles + k_tile_search with the fused aggregation"
-                                " + redo)") if gravnet else
-                               "binned_select_knn (k_tiles + k_tile_search + k_knn_fwd redo)",
+                     "kernel": ("knn_gravnet (k_tiles + k_tile_search + k_tile_finish + redo, then"
+                                " the aggregation)") if gravnet else
+                               "binned_select_knn (k_tiles + k_tile_search + k_tile_finish + "
+                               "k_knn_fwd redo)",
+                     "note": "achieved = the reference algorithm's bytes (SURVEY 8(d)) / time; "
+                             "frac > 1 means the kernels serve those candidate reads from "
+                             "L2/shared memory: traffic is what they take from DRAM",
                      "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": load_traffic(args.config),
                      "peak_source": peak_src,
