@@ -61,6 +61,9 @@ constexpr int kMaxSpanLen = 127;   // 7-bit offsets in the codes
 #ifndef FG_TILE_ALPHA
 #define FG_TILE_ALPHA 1.10f
 #endif
+#ifndef FG_RADIUS_ITERS
+#define FG_RADIUS_ITERS 2
+#endif
 constexpr float kAlpha = FG_TILE_ALPHA;  // radius inflation over the density estimate
 constexpr float kMargin = 1.0f + 1e-5f;
 constexpr float kSlackCells = 1e-4f;
@@ -934,7 +937,7 @@ __global__ void __launch_bounds__(kWarps * 32, SPLIT ? kScanCtasPerSm : kCtasPer
             near_face |= fminf(h0, (float)nb * w[i] - h0) < 3.0f * rad;
         }
 #pragma unroll 1
-        for (int it = 0; it < (__any_sync(FG_FULL_MASK, active && near_face) ? 3 : 0); ++it) {
+        for (int it = 0; it < (__any_sync(FG_FULL_MASK, active && near_face) ? FG_RADIUS_ITERS : 0); ++it) {
             float f = 1.0f;
 #pragma unroll
             for (int i = 0; i < DB; ++i) {
