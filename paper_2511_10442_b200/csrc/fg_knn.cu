@@ -253,12 +253,13 @@ extern "C" int fg_knn_gravnet_fwd_ws(const float* sorted_coords, const int32_t* 
                                      size_t workspace_bytes, void* stream) {
     // the fused op always returns float32 distances, no mask / radius
     if (flags & (FG_KNN_D2_F64 | FG_KNN_USE_DIRECTION | FG_KNN_USE_MAX_R2)) return FG_ERR_BAD_SHAPE;
-    FG_TRY(check_args(sorted_coords, sort_order, bin_idx, bin_bounds, row_splits, dim_mins, widths,
-                      n, n_coords, n_splits, d_bin, n_bins, k, nullptr, 0.0, flags, out_idx,
-                      out_d2));
+    if (k < 1 || k > 960) return FG_ERR_BAD_K;
     if (n_feats < 1 || !(weight_scale > 0.0)) return FG_ERR_BAD_SHAPE;
     unsigned bits = 0;
     FG_TRY(fg::gravnet::reducer_bits(reducers, n_reducers, &bits));
+    FG_TRY(check_args(sorted_coords, sort_order, bin_idx, bin_bounds, row_splits, dim_mins, widths,
+                      n, n_coords, n_splits, d_bin, n_bins, k, nullptr, 0.0, flags, out_idx,
+                      out_d2));
     if (n == 0) return 0;
     if (!feats || !agg_out) return FG_ERR_NULL;
     cudaStream_t st = (cudaStream_t)stream;

@@ -71,6 +71,17 @@ def test_validation_before_launch():
     assert L.fg_knn_workspace_size(1000, 5, 1, 4, 29, 40, 0, ctypes.byref(n)) == 0 and n.value == 0
     assert L.fg_knn_workspace_size(1000, 4, 1, 4, 29, 40, _lib.FG_KNN_NO_TILE,
                                    ctypes.byref(n)) == 0 and n.value == 0
+    # fused search + GravNet: float32 distances only, reducers validated before any launch
+    red = (ctypes.c_int32 * 2)(0, 1)
+    def kg(flags=0, k=40, n_feats=64, scale=10.0, reducers=red, n_red=2):
+        return L.fg_knn_gravnet_fwd_ws(None, None, None, None, None, None, None, 10, 4, 1, 4, 5, k,
+                                       flags, None, n_feats, scale, reducers, n_red, 1, None, None,
+                                       None, None, 0, None)
+    assert kg(flags=_lib.FG_KNN_D2_F64) == -2
+    assert kg(k=0) == -1
+    assert kg(scale=0.0) == -2
+    assert kg(n_red=5) == -2
+    assert kg() == -5  # NULL pointers
     for rc, exc in ((-1, errors.BadKError), (-3, errors.TooFewDimsError),
                     (-6, errors.BadShapeError), (-7, errors.BadKError)):
         with pytest.raises(exc):
