@@ -177,6 +177,7 @@ extern "C" int fg_knn_fwd_ws(const float* sorted_coords, const int32_t* sort_ord
     a.stats = nullptr;
     a.qlist = nullptr;
     a.qcount = nullptr;
+    a.qall = nullptr;
     if (flags & FG_KNN_STATS) {
         std::lock_guard<std::mutex> lk(g_stats_mu);
         if (!g_stats_dev) {
@@ -207,6 +208,7 @@ extern "C" int fg_knn_fwd_ws(const float* sorted_coords, const int32_t* sort_ord
         t.widths = widths;
         t.total = total;
         t.nb = n_bins;
+        t.n = n;
         t.k = k;
         t.nblk = (n_bins + 1) / 2;
         t.bps = (int)(w.n_blocks / n_splits);

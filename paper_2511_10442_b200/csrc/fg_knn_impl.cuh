@@ -95,6 +95,8 @@ struct KnnArgs {
     unsigned long long* stats;  // device counters (FG_KNN_STATS) or null
     const int32_t* qlist;       // optional query list (sorted positions), e.g. the
     const int* qcount;          // tile path's redo list; its length lives on the device
+    const int* qall;            // with qlist: *qall * 4 > n -> every query instead (the
+                                // tile kernels declined the data, fg_knn_tile.cuh)
 };
 
 template <int CAP>
@@ -906,9 +908,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, FG_KNN_MINB) k_knn_fwd(co
     const bool exhaustive = a.flags & FG_KNN_EXHAUSTIVE;
     Counters cnt;
     int64_t queries = 0;
-    const int64_t n_q = a.qlist ? (int64_t)*a.qcount : a.n;
+    const bool use_list = a.qlist && !(a.qall && (int64_t)*a.qall * 4 > a.n);
+    const int64_t n_q = use_list ? (int64_t)*a.qcount : a.n;
     for (int64_t i = warp_global; i < n_q; i += warps_total) {
-        const int64_t p = a.qlist ? (int64_t)a.qlist[i] : i;
+        const int64_t p = use_list ? (int64_t)a.qlist[i] : i;
         ++queries;
         const int32_t qid = a.sid[p];
         const int64_t row_out = (int64_t)qid * a.k;
@@ -952,7 +955,7 @@ int launch_knn(const KnnArgs& a, cudaStream_t st) {
     if (smem > 48 * 1024)
         FG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t blocks = std::min<int64_t>(ceil_div(a.n, kWarpsPerBlock),
-                                             a.qlist ? (int64_t)148 * 16 : (int64_t)1 << 30);
+                                             a.qlist ? (int64_t)148 * 64 : (int64_t)1 << 30);
     kern<<<(unsigned)blocks, kWarpsPerBlock * 32, smem, st>>>(a);
     return launched(st);
 }

@@ -11,7 +11,7 @@ namespace tile {
 
 template <int DB>
 int launch_db(TileArgs& t, const search::KnnArgs& a, cudaStream_t st) {
-    FG_CUDA(cudaMemsetAsync(t.ctr, 0, 4 * sizeof(int), st));
+    FG_CUDA(cudaMemsetAsync(t.ctr, 0, 8 * sizeof(int), st));
     k_tiles<DB><<<(unsigned)ceil_div(t.n_blocks, 4), 128, 0, st>>>(t);
     FG_TRY(launched(st));
     static int sms = 0;  // per template instance: also sets the smem opt-ins once
@@ -41,6 +41,7 @@ int launch_db(TileArgs& t, const search::KnnArgs& a, cudaStream_t st) {
     search::KnnArgs r = a;
     r.qlist = t.redo;
     r.qcount = &t.ctr[2];
+    r.qall = &t.ctr[4];
     return search::dispatch_db<1>(r, DB, st);
 }
 

@@ -83,7 +83,8 @@ struct TileArgs {
     int bps;           // lead blocks per split = nblk^(DB-1)
     int n_blocks;      // S * bps
     int2* tiles;       // (block id, c_lo | c_hi << 8 | count << 16)
-    int* ctr;          // [0] tiles, [1] tile cursor, [2] redo count
+    int* ctr;          // [0] tiles, [1] tile cursor, [2] redo count, [4] points in oversize columns
+    int64_t n;         // points (all splits)
     int32_t* redo;     // sorted positions left for the warp-per-query kernel
     int32_t* out_idx;
     float* out_d2;
@@ -187,6 +188,7 @@ __global__ void __launch_bounds__(128) k_tiles(const TileArgs a) {
         if (cnt > 0) {
             if (lane == nt) mine = make_int2(blk, start | (end << 8) | (min(cnt, 32767) << 16));
             ++nt;
+            if (cnt > 32 && lane == 0) atomicAdd(&a.ctr[4], cnt);  // clustered-data detector
         }
         base = pe;
         start = end + 1;
@@ -195,6 +197,14 @@ __global__ void __launch_bounds__(128) k_tiles(const TileArgs a) {
     if (lane == 0 && nt > 0) t0 = atomicAdd(&a.ctr[0], nt);
     t0 = __shfl_sync(FG_FULL_MASK, t0, 0);
     if (lane < nt) a.tiles[t0 + lane] = mine;
+}
+
+// More than a quarter of the points in columns too dense for a tile: the data
+// is clustered at the cell scale and the radius hint fails there; the tile
+// kernels step aside and the warp-per-query kernel takes every query in
+// sorted order (decided on the device, no host synchronisation).
+__device__ __forceinline__ bool tiles_declined(const TileArgs& a) {
+    return (int64_t)a.ctr[4] * 4 > a.n;
 }
 
 // ---------------------------------------------------------------- helpers
@@ -825,7 +835,7 @@ __global__ void __launch_bounds__(kWarps * 32, SPLIT ? kScanCtasPerSm : kCtasPer
     const int lane = lane_id();
     const int nb = a.nb;
     const int need = a.k - 1;
-    const int n_tiles = a.ctr[0];
+    const int n_tiles = tiles_declined(a) ? 0 : a.ctr[0];
     unsigned long long st_cand = 0, st_tiles = 0, st_redo = 0, st_fail = 0, st_exp = 0, st_eval = 0;
 
     for (;;) {
@@ -1156,6 +1166,7 @@ __global__ void __launch_bounds__(kFinishWarps * 32, FG_FINISH_MINB) k_tile_fini
     const int lane = lane_id();
     const int need = a.k - 1;
     unsigned long long st_redo = 0;
+    if (tiles_declined(a)) return;
     for (int64_t p = blockIdx.x * (int64_t)kFinishWarps + (threadIdx.x >> 5); p < n;
          p += (int64_t)gridDim.x * kFinishWarps) {
         const float2 mt = a.meta[p];

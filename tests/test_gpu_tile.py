@@ -55,7 +55,8 @@ def assert_oracle(O, c32, off, k):
 def test_tile_vs_oracle_uniform(oracle, d, k, S, seed):
     c, off = generate_dataset(12_000, d, S, seed, "uniform")
     st = assert_oracle(oracle, c.astype(np.float32), off, k)
-    assert st["tiles"] > 0  # the tile path actually ran
+    if d > 1:  # d = 1: 30 cells for 12k points -- the tile kernels decline (clustered rule)
+        assert st["tiles"] > 0  # the tile path actually ran
 
 
 def test_tile_ties_and_duplicates(oracle):
