@@ -47,7 +47,8 @@ enum fg_status {
     FG_ERR_WORKSPACE = -4,      /* workspace smaller than fg_*_workspace_size()         */
     FG_ERR_NULL = -5,           /* required pointer is NULL                             */
     FG_ERR_TOO_MANY_DIMS = -6,  /* n_coords > 16                                        */
-    FG_ERR_BAD_RADIUS = -7      /* max_radius2 < 0 (G/knn.py:57-58 BadKError)          */
+    FG_ERR_BAD_RADIUS = -7,     /* max_radius2 < 0 (G/knn.py:57-58 BadKError)          */
+    FG_ERR_BAD_CAPACITY = -8    /* n_maxuq / n_maxrs < 1 (G/ocgraph.py:176-179)         */
 };
 
 /* Option bits for fg_knn_fwd (mirror KnnOptions, G/knn.py:34-45, and the
@@ -195,6 +196,35 @@ int fg_gravnet_bwd(const float *feats, int64_t n, int32_t n_feats, const int32_t
                    int32_t n_reducers, int32_t include_self, const int32_t *order,
                    const float *upstream, float *grad_feats, float *grad_d2, void *workspace,
                    size_t workspace_bytes, void *stream);
+
+/* ---------------------------------------------------------------- association matrices */
+
+/* Scratch for fg_oc_find_unique over n vertices (hash table + flags + scan). */
+int fg_oc_unique_workspace_size(int64_t n, size_t *bytes);
+
+/* find_unique + max_same_count.  Replaces G/ocgraph.py:114-149: objects are
+ * the distinct non-negative ids per row split, in first-occurrence order.
+ * asso int64[n] (negative = background), row_splits int64[n_splits+1] (device).
+ * Writes unique_idx / unique_rs / counts (int64, capacity n; counts may be
+ * NULL) and summary int64[2] = {n_unique, largest member count} on the device. */
+int fg_oc_find_unique(const int64_t *asso, int64_t n, const int64_t *row_splits, int32_t n_splits,
+                      int64_t *unique_idx, int64_t *unique_rs, int64_t *counts, int64_t *summary,
+                      void *workspace, size_t workspace_bytes, void *stream);
+
+/* Scratch for fg_oc_matrices (per-object chunk counts). */
+int fg_oc_matrices_workspace_size(int64_t n_unique, int64_t max_window, size_t *bytes);
+
+/* oc_helper.  Replaces G/ocgraph.py:152-202 (the paper's Algorithm 3): for
+ * object i (unique_idx[i] in split unique_rs[i]) the window is the first
+ * n_maxrs vertices of its split; m[i] (int64[n_unique, n_maxuq]) gets the
+ * window's members ascending, truncated; m_not[i] (int64[n_unique, n_maxrs],
+ * NULL = calc_m_not False) the rest of the window ascending; -1 suffixes.
+ * visits (int64, device) = sum of window lengths.  max_window >= the largest
+ * row split size (sizes the grid).  Errors: FG_ERR_BAD_CAPACITY. */
+int fg_oc_matrices(const int64_t *asso, const int64_t *row_splits, int32_t n_splits,
+                   const int64_t *unique_idx, const int64_t *unique_rs, int64_t n_unique,
+                   int64_t n_maxuq, int64_t n_maxrs, int64_t max_window, int64_t *m, int64_t *m_not,
+                   int64_t *visits, void *workspace, size_t workspace_bytes, void *stream);
 
 /* ---------------------------------------------------------------- misc */
 

@@ -10,7 +10,7 @@ from __future__ import annotations
 import ctypes
 import os
 
-from .errors import (BackendUnavailableError, BadKError, BadShapeError, GridKnnError,
+from .errors import (BackendUnavailableError, BadCapacityError, BadKError, BadShapeError, GridKnnError,
                      ShapeMismatchError, TooFewDimsError)
 
 PKG = os.path.dirname(os.path.abspath(__file__))
@@ -34,7 +34,8 @@ EXPORTS = (
     "fg_knn_bwd_workspace_size", "fg_knn_bwd", "fg_gravnet_fwd",
     "fg_gravnet_bwd_workspace_size", "fg_gravnet_bwd", "fg_error_string", "fg_abi_version",
     "fg_launch_count", "fg_knn_stats", "fg_knn_workspace_size", "fg_knn_fwd_ws",
-    "fg_knn_gravnet_fwd_ws",
+    "fg_knn_gravnet_fwd_ws", "fg_oc_unique_workspace_size", "fg_oc_find_unique",
+    "fg_oc_matrices_workspace_size", "fg_oc_matrices",
 )
 
 _P = ctypes.c_void_p
@@ -64,6 +65,12 @@ _SIGS = {
                        ctypes.c_int),
     "fg_gravnet_bwd_workspace_size": ([_I64, _I32, _I32, _SZ], ctypes.c_int),
     "fg_gravnet_bwd": ([_P, _I64, _I32, _P, _P, _I32, _D, _P, _I32, _I32, _P, _P, _P, _P, _P,
+                        ctypes.c_size_t, _P], ctypes.c_int),
+    "fg_oc_unique_workspace_size": ([_I64, _SZ], ctypes.c_int),
+    "fg_oc_find_unique": ([_P, _I64, _P, _I32, _P, _P, _P, _P, _P, ctypes.c_size_t, _P],
+                          ctypes.c_int),
+    "fg_oc_matrices_workspace_size": ([_I64, _I64, _SZ], ctypes.c_int),
+    "fg_oc_matrices": ([_P, _P, _I32, _P, _P, _I64, _I64, _I64, _I64, _P, _P, _P, _P,
                         ctypes.c_size_t, _P], ctypes.c_int),
     "fg_error_string": ([ctypes.c_int], ctypes.c_char_p),
     "fg_abi_version": ([], ctypes.c_int),
@@ -110,6 +117,8 @@ def check(rc: int, what: str = "") -> None:
         raise BadShapeError(msg)
     if rc == -4:
         raise ShapeMismatchError(msg)
+    if rc == -8:
+        raise BadCapacityError(msg)
     raise GridKnnError(f"{msg} (code {rc})")
 
 

@@ -1,0 +1,343 @@
+// fg_oc.cu -- object-condensation association matrices (replaces
+// G/ocgraph.py:114-202: find_unique, max_same_count, oc_helper; the paper's
+// CUDA Algorithm 3) for sm_100a.
+//
+// find_unique: one pass inserts every non-background vertex's (id, split) key
+// into an open-addressing table with a 16-byte compare-and-swap (the key is
+// two 64-bit words: ids are opaque int64 labels), recording the first vertex
+// (atomicMin) and the member count per key.  A vertex is an object's first
+// occurrence iff it is its key's minimum; the exclusive scan of those flags in
+// vertex order is exactly the reference's object order (splits ascending,
+// first occurrence inside a split).
+//
+// oc_helper: a 2-d grid of (window chunk, object) blocks.  Pass 1 counts each
+// chunk's members; pass 2 re-reads the chunk (L2-resident: every object of a
+// split scans the same window), places members at prefix + block-scan rank
+// (truncated to n_maxuq) and non-members at (offset in window) - (members
+// before it), and fills the -1 suffixes.  Integer work throughout: bit-exact.
+#include "fg_common.cuh"
+#include "fg_scan.cuh"
+
+namespace fg {
+namespace oc {
+
+struct __align__(16) Key {
+    unsigned long long id, split;
+};
+constexpr unsigned long long kEmpty = ~0ull;
+constexpr int kThreads = 256;
+constexpr int kItems = 8;
+constexpr int kChunk = kThreads * kItems;
+
+__device__ __forceinline__ bool key_eq(const Key& a, const Key& b) { return a.id == b.id && a.split == b.split; }
+
+__device__ __forceinline__ int split_of(const int64_t* __restrict__ rs, int S, int64_t v) {
+    int lo = 0, hi = S;  // largest s with rs[s] <= v (empty splits skipped)
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (rs[mid] <= v) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ uint64_t mix(uint64_t x) {
+    x ^= x >> 33;
+    x *= 0xff51afd7ed558ccdull;
+    x ^= x >> 33;
+    x *= 0xc4ceb9fe1a85ec53ull;
+    x ^= x >> 33;
+    return x;
+}
+
+__global__ void k_oc_insert(const int64_t* __restrict__ asso, int64_t n, const int64_t* __restrict__ rs,
+                            int S, Key* __restrict__ table, uint64_t cap_mask,
+                            unsigned long long* __restrict__ first, unsigned long long* __restrict__ count,
+                            int64_t* __restrict__ slot_of) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t a = asso[v];
+        if (a < 0) {
+            slot_of[v] = -1;
+            continue;
+        }
+        const int s = split_of(rs, S, v);
+        const Key key{(unsigned long long)a, (unsigned long long)s};
+        const Key empty{kEmpty, kEmpty};
+        uint64_t h = mix((uint64_t)a * 0x9e3779b97f4a7c15ull + (uint64_t)s) & cap_mask;
+        for (;;) {
+            const Key old = atomicCAS(&table[h], empty, key);
+            if (key_eq(old, empty) || key_eq(old, key)) break;
+            h = (h + 1) & cap_mask;
+        }
+        atomicMin(&first[h], (unsigned long long)v);
+        atomicAdd(&count[h], 1ull);
+        slot_of[v] = (int64_t)h;
+    }
+}
+
+__global__ void k_oc_flag(const int64_t* __restrict__ slot_of, int64_t n,
+                          const unsigned long long* __restrict__ first, int32_t* __restrict__ flag) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t h = slot_of[v];
+        flag[v] = (h >= 0 && first[h] == (unsigned long long)v) ? 1 : 0;
+    }
+}
+
+// summary[0] = number of objects, summary[1] = largest member count
+__global__ void k_oc_emit(const int64_t* __restrict__ asso, int64_t n, const int64_t* __restrict__ rs, int S,
+                          const int64_t* __restrict__ slot_of, const int32_t* __restrict__ flag,
+                          const int32_t* __restrict__ excl, const unsigned long long* __restrict__ count,
+                          int64_t* __restrict__ unique_idx, int64_t* __restrict__ unique_rs,
+                          int64_t* __restrict__ counts, int64_t* __restrict__ summary) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        if (v == 0) summary[0] = excl[n];
+        if (!flag[v]) continue;
+        const int64_t o = excl[v];
+        const unsigned long long c = count[slot_of[v]];
+        unique_idx[o] = asso[v];
+        unique_rs[o] = split_of(rs, S, v);
+        if (counts) counts[o] = (int64_t)c;
+        atomicMax((unsigned long long*)&summary[1], c);
+    }
+}
+
+// ---------------------------------------------------------------- matrices
+struct MatArgs {
+    const int64_t* asso;
+    const int64_t* rs;
+    const int64_t* uidx;
+    const int64_t* urs;
+    int64_t n_u, n_maxuq, n_maxrs;
+    int n_chunks;
+    int32_t* cnt;  // [n_u][n_chunks]
+    int64_t* m;
+    int64_t* m_not;
+    unsigned long long* visits;
+};
+
+__device__ __forceinline__ void window_of(const MatArgs& a, int64_t i, int64_t& start, int64_t& len) {
+    const int s = (int)a.urs[i];
+    start = a.rs[s];
+    len = min(a.rs[s + 1] - start, a.n_maxrs);
+}
+
+__global__ void __launch_bounds__(kThreads) k_oc_count(const MatArgs a) {
+  __shared__ int s_w[kThreads / 32];
+  for (int64_t i = blockIdx.y; i < a.n_u; i += gridDim.y) {
+    int64_t start, len;
+    window_of(a, i, start, len);
+    const int64_t obj = a.uidx[i];
+    const int64_t c0 = (int64_t)blockIdx.x * kChunk;
+    int c = 0;
+    if (c0 < len) {
+#pragma unroll
+        for (int j = 0; j < kItems; ++j) {
+            const int64_t o = c0 + j * kThreads + threadIdx.x;  // coalesced
+            c += (o < len && a.asso[start + o] == obj) ? 1 : 0;
+        }
+    }
+    c = __reduce_add_sync(FG_FULL_MASK, c);
+    if (lane_id() == 0) s_w[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+#pragma unroll
+        for (int w = 0; w < kThreads / 32; ++w) t += s_w[w];
+        a.cnt[i * a.n_chunks + blockIdx.x] = t;
+        if (blockIdx.x == 0) atomicAdd(a.visits, (unsigned long long)len);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_oc_write(const MatArgs a) {
+  __shared__ int64_t s_pre, s_tot;
+  __shared__ int s_w[kThreads / 32];
+  for (int64_t i = blockIdx.y; i < a.n_u; i += gridDim.y) {
+    int64_t start, len;
+    window_of(a, i, start, len);
+    const int64_t obj = a.uidx[i];
+    const int64_t c0 = (int64_t)blockIdx.x * kChunk;
+    if (threadIdx.x < 32) {  // members before this chunk and in the whole window
+        int64_t pre = 0, tot = 0;
+        for (int c = threadIdx.x; c < a.n_chunks; c += 32) {
+            const int64_t x = a.cnt[i * a.n_chunks + c];
+            tot += x;
+            pre += c < (int)blockIdx.x ? x : 0;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            pre += __shfl_xor_sync(FG_FULL_MASK, pre, o);
+            tot += __shfl_xor_sync(FG_FULL_MASK, tot, o);
+        }
+        if (threadIdx.x == 0) {
+            s_pre = pre;
+            s_tot = tot;
+        }
+    }
+    // this thread's kItems consecutive vertices of the chunk
+    const int64_t t0 = c0 + (int64_t)threadIdx.x * kItems;
+    bool mem[kItems];
+    int c = 0;
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+        const int64_t o = t0 + j;
+        mem[j] = o < len && a.asso[start + o] == obj;
+        c += mem[j] ? 1 : 0;
+    }
+    const int incl = warp_inclusive_scan(c);
+    if (lane_id() == 31) s_w[threadIdx.x >> 5] = incl;
+    __syncthreads();
+    int before = incl - c;
+    for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) before += s_w[w];
+    int64_t r = s_pre + before;  // members of the window before vertex t0
+    int64_t* mrow = a.m + i * a.n_maxuq;
+    int64_t* nrow = a.m_not ? a.m_not + i * a.n_maxrs : nullptr;
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+        const int64_t o = t0 + j;
+        if (o >= len) break;
+        if (mem[j]) {
+            if (r < a.n_maxuq) mrow[r] = start + o;
+            ++r;
+        } else if (nrow) {
+            nrow[o - r] = start + o;  // o - r non-members precede it
+        }
+    }
+    // -1 suffixes, shared by the object's blocks
+    const int64_t m_fill = min(s_tot, a.n_maxuq);
+    const int64_t stride = (int64_t)gridDim.x * kThreads;
+    for (int64_t x = m_fill + blockIdx.x * (int64_t)kThreads + threadIdx.x; x < a.n_maxuq; x += stride) mrow[x] = -1;
+    if (nrow) {
+        for (int64_t x = (len - s_tot) + blockIdx.x * (int64_t)kThreads + threadIdx.x; x < a.n_maxrs; x += stride)
+            nrow[x] = -1;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace oc
+}  // namespace fg
+
+using namespace fg;
+using namespace fg::oc;
+
+namespace {
+uint64_t table_cap(int64_t n) {
+    uint64_t c = 1024;
+    while (c < 2 * (uint64_t)n) c <<= 1;
+    return c;
+}
+size_t n_scan_tiles(int64_t n) { return (size_t)ceil_div(n, (int64_t)kScanTile); }
+
+struct UniqueWs {
+    Key* table;
+    unsigned long long *first, *count;
+    int64_t* slot_of;
+    int32_t *flag, *excl, *cursor;
+    unsigned long long* status;
+    unsigned* ticket;
+    size_t bytes;
+};
+
+UniqueWs carve_unique(void* base, int64_t n) {
+    UniqueWs w{};
+    const uint64_t cap = table_cap(n);
+    char* p = (char*)base;
+    size_t off = 0;
+    auto take = [&](size_t b) {
+        void* r = p ? p + off : nullptr;
+        off += align_up(b, 256);
+        return r;
+    };
+    w.table = (Key*)take(sizeof(Key) * cap);
+    w.first = (unsigned long long*)take(8 * cap);
+    w.count = (unsigned long long*)take(8 * cap);
+    w.slot_of = (int64_t*)take(8 * (size_t)n);
+    w.flag = (int32_t*)take(4 * (size_t)n);
+    w.excl = (int32_t*)take(4 * ((size_t)n + 1));
+    w.cursor = (int32_t*)take(4 * (size_t)n);
+    w.status = (unsigned long long*)take(8 * (n_scan_tiles(n) + 1));
+    w.ticket = (unsigned*)take(16);
+    w.bytes = off;
+    return w;
+}
+}  // namespace
+
+extern "C" int fg_oc_unique_workspace_size(int64_t n, size_t* bytes) {
+    if (!bytes) return FG_ERR_NULL;
+    if (n < 0 || n > INT32_MAX - 1) return FG_ERR_BAD_SHAPE;
+    *bytes = carve_unique(nullptr, n).bytes;
+    return 0;
+}
+
+extern "C" int fg_oc_find_unique(const int64_t* asso, int64_t n, const int64_t* row_splits, int32_t n_splits,
+                                 int64_t* unique_idx, int64_t* unique_rs, int64_t* counts, int64_t* summary,
+                                 void* workspace, size_t workspace_bytes, void* stream) {
+    if (n < 0 || n > INT32_MAX - 1 || n_splits < 1) return FG_ERR_BAD_SHAPE;
+    if (!row_splits || !summary) return FG_ERR_NULL;
+    cudaStream_t st = (cudaStream_t)stream;
+    FG_CUDA(cudaMemsetAsync(summary, 0, 2 * sizeof(int64_t), st));
+    if (n == 0) return 0;
+    if (!asso || !unique_idx || !unique_rs || !workspace) return FG_ERR_NULL;
+    UniqueWs w = carve_unique(workspace, n);
+    if (workspace_bytes < w.bytes) return FG_ERR_WORKSPACE;
+    const uint64_t cap = table_cap(n);
+    FG_CUDA(cudaMemsetAsync(w.table, 0xff, sizeof(Key) * cap, st));
+    FG_CUDA(cudaMemsetAsync(w.first, 0xff, 8 * cap, st));
+    FG_CUDA(cudaMemsetAsync(w.count, 0, 8 * cap, st));
+    FG_CUDA(cudaMemsetAsync(w.status, 0, 8 * (n_scan_tiles(n) + 1), st));
+    FG_CUDA(cudaMemsetAsync(w.ticket, 0, 16, st));
+    const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(n, (int64_t)256), 148 * 16);
+    k_oc_insert<<<blocks, 256, 0, st>>>(asso, n, row_splits, n_splits, w.table, cap - 1, w.first, w.count,
+                                        w.slot_of);
+    FG_TRY(launched(st));
+    k_oc_flag<<<blocks, 256, 0, st>>>(w.slot_of, n, w.first, w.flag);
+    FG_TRY(launched(st));
+    k_scan<<<(unsigned)n_scan_tiles(n), kScanThreads, 0, st>>>(w.flag, n, w.excl, w.cursor, w.status, w.ticket);
+    FG_TRY(launched(st));
+    k_oc_emit<<<blocks, 256, 0, st>>>(asso, n, row_splits, n_splits, w.slot_of, w.flag, w.excl, w.count,
+                                      unique_idx, unique_rs, counts, summary);
+    return launched(st);
+}
+
+extern "C" int fg_oc_matrices_workspace_size(int64_t n_unique, int64_t max_window, size_t* bytes) {
+    if (!bytes) return FG_ERR_NULL;
+    if (n_unique < 0 || max_window < 0) return FG_ERR_BAD_SHAPE;
+    const int64_t chunks = std::max<int64_t>(1, ceil_div(max_window, (int64_t)kChunk));
+    *bytes = align_up(sizeof(int32_t) * (size_t)(n_unique * chunks), 256) + 256;
+    return 0;
+}
+
+extern "C" int fg_oc_matrices(const int64_t* asso, const int64_t* row_splits, int32_t n_splits,
+                              const int64_t* unique_idx, const int64_t* unique_rs, int64_t n_unique,
+                              int64_t n_maxuq, int64_t n_maxrs, int64_t max_window, int64_t* m, int64_t* m_not,
+                              int64_t* visits, void* workspace, size_t workspace_bytes, void* stream) {
+    if (n_maxuq < 1 || n_maxrs < 1) return FG_ERR_BAD_CAPACITY;
+    if (n_unique < 0 || max_window < 0 || n_splits < 1) return FG_ERR_BAD_SHAPE;
+    if (!visits) return FG_ERR_NULL;
+    cudaStream_t st = (cudaStream_t)stream;
+    FG_CUDA(cudaMemsetAsync(visits, 0, sizeof(int64_t), st));
+    if (n_unique == 0) return 0;
+    if (!asso || !row_splits || !unique_idx || !unique_rs || !m || !workspace) return FG_ERR_NULL;
+    size_t need = 0;
+    FG_TRY(fg_oc_matrices_workspace_size(n_unique, max_window, &need));
+    if (workspace_bytes < need) return FG_ERR_WORKSPACE;
+    MatArgs a{};
+    a.asso = asso;
+    a.rs = row_splits;
+    a.uidx = unique_idx;
+    a.urs = unique_rs;
+    a.n_u = n_unique;
+    a.n_maxuq = n_maxuq;
+    a.n_maxrs = n_maxrs;
+    a.n_chunks = (int)std::max<int64_t>(1, ceil_div(std::min(max_window, n_maxrs), (int64_t)kChunk));
+    a.cnt = (int32_t*)workspace;
+    a.m = m;
+    a.m_not = m_not;
+    a.visits = (unsigned long long*)visits;
+    const dim3 grid((unsigned)a.n_chunks, (unsigned)std::min<int64_t>(n_unique, 65535));
+    k_oc_count<<<grid, kThreads, 0, st>>>(a);
+    FG_TRY(launched(st));
+    k_oc_write<<<grid, kThreads, 0, st>>>(a);
+    return launched(st);
+}

@@ -391,3 +391,55 @@ def _kg_backward(ctx, grad_idx, grad_d2, grad_agg):
 
 
 knn_gravnet.register_autograd(_kg_backward, setup_context=_kg_setup)
+
+
+# ---------------------------------------------------------------- association matrices
+# Object counts are data dependent (the result size is read back once), so these
+# two are plain functions over the C ABI rather than traceable torch.library ops.
+def oc_find_unique(asso: Tensor, row_splits: Tensor):
+    """find_unique + max_same_count (G/ocgraph.py:114-149) on the device.
+
+    asso i64[N] (negative = background), row_splits i64[S+1] ->
+    (unique_idx i64[U], unique_rs i64[U], counts i64[U], max_count int)."""
+    _require_cuda(asso, row_splits)
+    a = asso.to(torch.int64).contiguous()
+    rs = row_splits.to(device=a.device, dtype=torch.int64).contiguous()
+    n, S = a.numel(), rs.numel() - 1
+    if S < 1:
+        raise BadShapeError("row_splits needs at least 2 entries")
+    L = _lib.load()
+    ws = _ws(_lib.size_out(L.fg_oc_unique_workspace_size, n), a.device)
+    uidx = torch.empty(max(n, 1), dtype=torch.int64, device=a.device)
+    urs = torch.empty_like(uidx)
+    cnt = torch.empty_like(uidx)
+    summary = torch.empty(2, dtype=torch.int64, device=a.device)
+    _lib.check(L.fg_oc_find_unique(_p(a), n, _p(rs), S, _p(uidx), _p(urs), _p(cnt), _p(summary),
+                                   _p(ws), ws.numel(), _stream(a)), "find_unique")
+    n_u, top = (int(x) for x in summary.cpu())
+    return uidx[:n_u], urs[:n_u], cnt[:n_u], top
+
+
+def oc_matrices(asso: Tensor, row_splits: Tensor, unique_idx: Tensor, unique_rs: Tensor,
+                n_maxuq: int, n_maxrs: int, max_window: int, calc_m_not: bool = True):
+    """oc_helper's M / M-not rows (G/ocgraph.py:152-202) on the device ->
+    (m i64[U, n_maxuq], m_not i64[U, n_maxrs] or None, visits i64[1] device)."""
+    _require_cuda(asso, row_splits, unique_idx, unique_rs)
+    a = asso.to(torch.int64).contiguous()
+    rs = row_splits.to(device=a.device, dtype=torch.int64).contiguous()
+    ui = unique_idx.to(device=a.device, dtype=torch.int64).contiguous()
+    ur = unique_rs.to(device=a.device, dtype=torch.int64).contiguous()
+    if ui.numel() != ur.numel():
+        raise BadShapeError("unique ids and splits must be equally long")
+    n_u = ui.numel()
+    L = _lib.load()
+    if n_maxuq < 1 or n_maxrs < 1:  # validated by the library before any launch
+        _lib.check(L.fg_oc_matrices(None, None, 1, None, None, 0, int(n_maxuq), int(n_maxrs), 0,
+                                    None, None, None, None, 0, None), "oc_helper")
+    ws = _ws(_lib.size_out(L.fg_oc_matrices_workspace_size, n_u, int(max_window)), a.device)
+    m = torch.empty((n_u, int(n_maxuq)), dtype=torch.int64, device=a.device)
+    m_not = torch.empty((n_u, int(n_maxrs)), dtype=torch.int64, device=a.device) if calc_m_not else None
+    visits = torch.empty(1, dtype=torch.int64, device=a.device)
+    _lib.check(L.fg_oc_matrices(_p(a), _p(rs), rs.numel() - 1, _p(ui), _p(ur), n_u, int(n_maxuq),
+                                int(n_maxrs), int(max_window), _p(m), _p(m_not), _p(visits), _p(ws),
+                                ws.numel(), _stream(a)), "oc_helper")
+    return m, m_not, visits

@@ -47,3 +47,26 @@ def golden_case(g, name):
                                            "knn_idx_sorted", "knn_d2_sorted", "brute_k1_idx",
                                            "brute_k1_d2", "upstream", "grad_raw_rows")},
     }
+
+
+GOLDEN_OC = os.path.join(ROOT, "tests", "golden", "reference_oc.npz")
+
+
+@pytest.fixture(scope="session")
+def golden_oc():
+    return np.load(GOLDEN_OC)
+
+
+def oc_case(g, name):
+    """One association batch + the reference's find_unique / oc_helper outputs
+    (tests/golden/make_golden_oc.py)."""
+    pre = f"{name}__"
+    caps = g[pre + "caps"]
+    return {
+        "asso": g[pre + "asso"], "row_splits": g[pre + "row_splits"],
+        "n_maxuq": None if caps[0] < 0 else int(caps[0]),
+        "n_maxrs": None if caps[1] < 0 else int(caps[1]),
+        "cap_uq": int(caps[2]), "cap_rs": int(caps[3]), "visits": int(caps[4]),
+        "top": int(caps[5]),
+        **{key: g[pre + key] for key in ("unique_idx", "unique_rs", "counts", "m", "m_not")},
+    }

@@ -82,7 +82,14 @@ def test_validation_before_launch():
     assert kg(scale=0.0) == -2
     assert kg(n_red=5) == -2
     assert kg() == -5  # NULL pointers
-    for rc, exc in ((-1, errors.BadKError), (-3, errors.TooFewDimsError),
+    # association matrices: capacities checked first, then pointers
+    assert L.fg_oc_matrices(None, None, 1, None, None, 3, 0, 5, 10, None, None, None, None, 0,
+                            None) == -8
+    assert L.fg_oc_matrices(None, None, 1, None, None, 3, 4, 5, 10, None, None, None, None, 0,
+                            None) == -5
+    assert L.fg_oc_unique_workspace_size(1000, ctypes.byref(n)) == 0 and n.value > 16 * 1000
+    assert L.fg_oc_matrices_workspace_size(10, 5000, ctypes.byref(n)) == 0 and n.value >= 120
+    for rc, exc in ((-8, errors.BadCapacityError), (-1, errors.BadKError), (-3, errors.TooFewDimsError),
                     (-6, errors.BadShapeError), (-7, errors.BadKError)):
         with pytest.raises(exc):
             _lib.check(rc)
