@@ -26,7 +26,10 @@ struct __align__(16) Key {
 };
 constexpr unsigned long long kEmpty = ~0ull;
 constexpr int kThreads = 256;
-constexpr int kItems = 8;
+#ifndef FG_OC_ITEMS
+#define FG_OC_ITEMS 8
+#endif
+constexpr int kItems = FG_OC_ITEMS;
 constexpr int kChunk = kThreads * kItems;
 
 __device__ __forceinline__ bool key_eq(const Key& a, const Key& b) { return a.id == b.id && a.split == b.split; }
@@ -151,15 +154,16 @@ __global__ void __launch_bounds__(kThreads) k_oc_count(const MatArgs a) {
 
 __global__ void __launch_bounds__(kThreads) k_oc_write(const MatArgs a) {
   __shared__ int64_t s_pre, s_tot;
-  __shared__ int s_w[kThreads / 32];
+  __shared__ int s_cnt[kItems * (kThreads / 32)];
+  static_assert(kItems * (kThreads / 32) % 32 == 0, "scan layout");
   for (int64_t i = blockIdx.y; i < a.n_u; i += gridDim.y) {
     int64_t start, len;
     window_of(a, i, start, len);
     const int64_t obj = a.uidx[i];
     const int64_t c0 = (int64_t)blockIdx.x * kChunk;
-    if (threadIdx.x < 32) {  // members before this chunk and in the whole window
+    if (threadIdx.x >= kThreads - 32) {  // members before this chunk and in the whole window
         int64_t pre = 0, tot = 0;
-        for (int c = threadIdx.x; c < a.n_chunks; c += 32) {
+        for (int c = threadIdx.x & 31; c < a.n_chunks; c += 32) {
             const int64_t x = a.cnt[i * a.n_chunks + c];
             tot += x;
             pre += c < (int)blockIdx.x ? x : 0;
@@ -169,36 +173,58 @@ __global__ void __launch_bounds__(kThreads) k_oc_write(const MatArgs a) {
             pre += __shfl_xor_sync(FG_FULL_MASK, pre, o);
             tot += __shfl_xor_sync(FG_FULL_MASK, tot, o);
         }
-        if (threadIdx.x == 0) {
+        if (threadIdx.x == kThreads - 32) {
             s_pre = pre;
             s_tot = tot;
         }
     }
-    // this thread's kItems consecutive vertices of the chunk
-    const int64_t t0 = c0 + (int64_t)threadIdx.x * kItems;
-    bool mem[kItems];
-    int c = 0;
+    // item j of this thread = vertex c0 + j*kThreads + tid (coalesced loads and,
+    // since ranks advance by at most one per lane, near-coalesced stores); the
+    // rank of a vertex = members before it in (item, warp, lane) order
+    const int lane = lane_id(), w = threadIdx.x >> 5;
+    unsigned bal[kItems];
+    const int o0 = (int)c0 + (int)threadIdx.x;  // window offsets fit in 32 bits
+    const int len32 = (int)len;
+    const int64_t* src = a.asso + start + o0;
 #pragma unroll
-    for (int j = 0; j < kItems; ++j) {
-        const int64_t o = t0 + j;
-        mem[j] = o < len && a.asso[start + o] == obj;
-        c += mem[j] ? 1 : 0;
+    for (int j = 0; j < kItems; ++j)
+        bal[j] = __ballot_sync(FG_FULL_MASK, o0 + j * kThreads < len32 && src[j * kThreads] == obj);
+    if (lane < kItems) {
+        unsigned b = 0;
+#pragma unroll
+        for (int j = 0; j < kItems; ++j) b = lane == j ? bal[j] : b;
+        s_cnt[lane * (kThreads / 32) + w] = __popc(b);
     }
-    const int incl = warp_inclusive_scan(c);
-    if (lane_id() == 31) s_w[threadIdx.x >> 5] = incl;
     __syncthreads();
-    int before = incl - c;
-    for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) before += s_w[w];
-    int64_t r = s_pre + before;  // members of the window before vertex t0
+    if (w == 0) {  // exclusive scan of the kItems x warps counts, item-major
+        constexpr int P = kItems * (kThreads / 32) / 32;
+        int v[P], run = 0;
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            v[q] = s_cnt[lane * P + q];
+            run += v[q];
+        }
+        const int incl = warp_inclusive_scan(run);
+        int ex = incl - run;
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            s_cnt[lane * P + q] = ex;
+            ex += v[q];
+        }
+    }
+    __syncthreads();
     int64_t* mrow = a.m + i * a.n_maxuq;
     int64_t* nrow = a.m_not ? a.m_not + i * a.n_maxrs : nullptr;
+    const int pre = (int)s_pre;
+    const int cap_uq = (int)min(a.n_maxuq, (int64_t)INT32_MAX);
+    const unsigned below = lanemask_lt();
 #pragma unroll
     for (int j = 0; j < kItems; ++j) {
-        const int64_t o = t0 + j;
-        if (o >= len) break;
-        if (mem[j]) {
-            if (r < a.n_maxuq) mrow[r] = start + o;
-            ++r;
+        const int o = o0 + j * kThreads;
+        if (o >= len32) break;
+        const int r = pre + s_cnt[j * (kThreads / 32) + w] + __popc(bal[j] & below);
+        if ((bal[j] >> lane) & 1u) {
+            if (r < cap_uq) mrow[r] = start + o;
         } else if (nrow) {
             nrow[o - r] = start + o;  // o - r non-members precede it
         }
@@ -313,7 +339,8 @@ extern "C" int fg_oc_matrices(const int64_t* asso, const int64_t* row_splits, in
                               int64_t n_maxuq, int64_t n_maxrs, int64_t max_window, int64_t* m, int64_t* m_not,
                               int64_t* visits, void* workspace, size_t workspace_bytes, void* stream) {
     if (n_maxuq < 1 || n_maxrs < 1) return FG_ERR_BAD_CAPACITY;
-    if (n_unique < 0 || max_window < 0 || n_splits < 1) return FG_ERR_BAD_SHAPE;
+    if (n_unique < 0 || max_window < 0 || max_window > INT32_MAX - 2 * kChunk || n_splits < 1)
+        return FG_ERR_BAD_SHAPE;
     if (!visits) return FG_ERR_NULL;
     cudaStream_t st = (cudaStream_t)stream;
     FG_CUDA(cudaMemsetAsync(visits, 0, sizeof(int64_t), st));
