@@ -52,28 +52,38 @@ __device__ __forceinline__ uint64_t mix(uint64_t x) {
     return x;
 }
 
+// Lanes holding the same key (consecutive vertices of one object) are merged
+// first (match_any): one table operation per group, the group's lowest
+// vertex and size.
 __global__ void k_oc_insert(const int64_t* __restrict__ asso, int64_t n, const int64_t* __restrict__ rs,
                             int S, Key* __restrict__ table, uint64_t cap_mask,
                             unsigned long long* __restrict__ first, unsigned long long* __restrict__ count,
                             int64_t* __restrict__ slot_of) {
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t a = asso[v];
-        if (a < 0) {
-            slot_of[v] = -1;
-            continue;
+    const int lane = lane_id();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); b < n; b += stride) {
+        const int64_t v = b + lane;  // b is warp-uniform: the match below sees the whole warp
+        const int64_t a = v < n ? asso[v] : -1;
+        const int s = a >= 0 ? split_of(rs, S, v) : -1;
+        const unsigned grp = __match_any_sync(FG_FULL_MASK, (unsigned long long)a) &
+                             __match_any_sync(FG_FULL_MASK, s);
+        const int leader = __ffs(grp) - 1;
+        int64_t h = -1;
+        if (a >= 0 && lane == leader) {
+            const Key key{(unsigned long long)a, (unsigned long long)s};
+            const Key empty{kEmpty, kEmpty};
+            uint64_t t = mix((uint64_t)a * 0x9e3779b97f4a7c15ull + (uint64_t)s) & cap_mask;
+            for (;;) {
+                const Key old = atomicCAS(&table[t], empty, key);
+                if (key_eq(old, empty) || key_eq(old, key)) break;
+                t = (t + 1) & cap_mask;
+            }
+            atomicMin(&first[t], (unsigned long long)v);  // lowest vertex of the group
+            atomicAdd(&count[t], (unsigned long long)__popc(grp));
+            h = (int64_t)t;
         }
-        const int s = split_of(rs, S, v);
-        const Key key{(unsigned long long)a, (unsigned long long)s};
-        const Key empty{kEmpty, kEmpty};
-        uint64_t h = mix((uint64_t)a * 0x9e3779b97f4a7c15ull + (uint64_t)s) & cap_mask;
-        for (;;) {
-            const Key old = atomicCAS(&table[h], empty, key);
-            if (key_eq(old, empty) || key_eq(old, key)) break;
-            h = (h + 1) & cap_mask;
-        }
-        atomicMin(&first[h], (unsigned long long)v);
-        atomicAdd(&count[h], 1ull);
-        slot_of[v] = (int64_t)h;
+        h = __shfl_sync(FG_FULL_MASK, h, leader);
+        if (v < n) slot_of[v] = a >= 0 ? h : -1;
     }
 }
 
@@ -110,8 +120,9 @@ struct MatArgs {
     const int64_t* uidx;
     const int64_t* urs;
     int64_t n_u, n_maxuq, n_maxrs;
-    int n_chunks;
-    int32_t* cnt;  // [n_u][n_chunks]
+    int n_chunks;                  // chunks of the largest window
+    unsigned long long* status;    // [n_u][n_chunks] look-back words
+    unsigned* ticket;
     int64_t* m;
     int64_t* m_not;
     unsigned long long* visits;
@@ -123,69 +134,35 @@ __device__ __forceinline__ void window_of(const MatArgs& a, int64_t i, int64_t& 
     len = min(a.rs[s + 1] - start, a.n_maxrs);
 }
 
-__global__ void __launch_bounds__(kThreads) k_oc_count(const MatArgs a) {
-  __shared__ int s_w[kThreads / 32];
-  for (int64_t i = blockIdx.y; i < a.n_u; i += gridDim.y) {
+// One block per (object, window chunk), in ticket order so every block's
+// predecessors have started: members of the chunk are ranked by ballots, the
+// members before the chunk come from a decoupled look-back over the object's
+// earlier chunks (flag 1 = chunk count, flag 2 = inclusive prefix), and the
+// object's last chunk fills the -1 suffixes.
+__global__ void __launch_bounds__(kThreads) k_oc_rows(const MatArgs a) {
+    __shared__ int s_cnt[kItems * (kThreads / 32)];
+    __shared__ int s_pre, s_tot;
+    __shared__ unsigned s_tile;
+    static_assert(kItems * (kThreads / 32) % 32 == 0, "scan layout");
+    if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1u);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int64_t i = tile / a.n_chunks;
+    const int c = (int)(tile - i * a.n_chunks);
     int64_t start, len;
     window_of(a, i, start, len);
+    const int n_ch = max(1, (int)((len + kChunk - 1) / kChunk));  // this object's chunks
+    if (c >= n_ch) return;                                  // past its window (uniform)
+    if (c == 0 && threadIdx.x == 0) atomicAdd(a.visits, (unsigned long long)len);
     const int64_t obj = a.uidx[i];
-    const int64_t c0 = (int64_t)blockIdx.x * kChunk;
-    int c = 0;
-    if (c0 < len) {
-#pragma unroll
-        for (int j = 0; j < kItems; ++j) {
-            const int64_t o = c0 + j * kThreads + threadIdx.x;  // coalesced
-            c += (o < len && a.asso[start + o] == obj) ? 1 : 0;
-        }
-    }
-    c = __reduce_add_sync(FG_FULL_MASK, c);
-    if (lane_id() == 0) s_w[threadIdx.x >> 5] = c;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int t = 0;
-#pragma unroll
-        for (int w = 0; w < kThreads / 32; ++w) t += s_w[w];
-        a.cnt[i * a.n_chunks + blockIdx.x] = t;
-        if (blockIdx.x == 0) atomicAdd(a.visits, (unsigned long long)len);
-    }
-    __syncthreads();
-  }
-}
-
-__global__ void __launch_bounds__(kThreads) k_oc_write(const MatArgs a) {
-  __shared__ int64_t s_pre, s_tot;
-  __shared__ int s_cnt[kItems * (kThreads / 32)];
-  static_assert(kItems * (kThreads / 32) % 32 == 0, "scan layout");
-  for (int64_t i = blockIdx.y; i < a.n_u; i += gridDim.y) {
-    int64_t start, len;
-    window_of(a, i, start, len);
-    const int64_t obj = a.uidx[i];
-    const int64_t c0 = (int64_t)blockIdx.x * kChunk;
-    if (threadIdx.x >= kThreads - 32) {  // members before this chunk and in the whole window
-        int64_t pre = 0, tot = 0;
-        for (int c = threadIdx.x & 31; c < a.n_chunks; c += 32) {
-            const int64_t x = a.cnt[i * a.n_chunks + c];
-            tot += x;
-            pre += c < (int)blockIdx.x ? x : 0;
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            pre += __shfl_xor_sync(FG_FULL_MASK, pre, o);
-            tot += __shfl_xor_sync(FG_FULL_MASK, tot, o);
-        }
-        if (threadIdx.x == kThreads - 32) {
-            s_pre = pre;
-            s_tot = tot;
-        }
-    }
+    const int lane = lane_id(), w = threadIdx.x >> 5;
     // item j of this thread = vertex c0 + j*kThreads + tid (coalesced loads and,
     // since ranks advance by at most one per lane, near-coalesced stores); the
     // rank of a vertex = members before it in (item, warp, lane) order
-    const int lane = lane_id(), w = threadIdx.x >> 5;
-    unsigned bal[kItems];
-    const int o0 = (int)c0 + (int)threadIdx.x;  // window offsets fit in 32 bits
+    const int o0 = c * kChunk + (int)threadIdx.x;  // window offsets fit in 32 bits
     const int len32 = (int)len;
     const int64_t* src = a.asso + start + o0;
+    unsigned bal[kItems];
 #pragma unroll
     for (int j = 0; j < kItems; ++j)
         bal[j] = __ballot_sync(FG_FULL_MASK, o0 + j * kThreads < len32 && src[j * kThreads] == obj);
@@ -196,7 +173,7 @@ __global__ void __launch_bounds__(kThreads) k_oc_write(const MatArgs a) {
         s_cnt[lane * (kThreads / 32) + w] = __popc(b);
     }
     __syncthreads();
-    if (w == 0) {  // exclusive scan of the kItems x warps counts, item-major
+    if (w == 0) {  // exclusive scan of the kItems x warps counts, then the look-back
         constexpr int P = kItems * (kThreads / 32) / 32;
         int v[P], run = 0;
 #pragma unroll
@@ -211,11 +188,43 @@ __global__ void __launch_bounds__(kThreads) k_oc_write(const MatArgs a) {
             s_cnt[lane * P + q] = ex;
             ex += v[q];
         }
+        const int total = __shfl_sync(FG_FULL_MASK, incl, 31);
+        unsigned long long* st = a.status + i * a.n_chunks;
+        int prefix = 0;
+        if (c == 0) {
+            if (lane == 0) atomicExch(&st[0], (2ull << 62) | (unsigned)total);
+        } else {
+            if (lane == 0) atomicExch(&st[c], (1ull << 62) | (unsigned)total);
+            int end = c - 1;
+            for (;;) {
+                const int idx = end - lane;
+                unsigned long long word = 2ull << 62;  // before chunk 0: prefix 0
+                if (idx >= 0) {
+                    do {
+                        word = *((volatile unsigned long long*)&st[idx]);
+                    } while ((word >> 62) == 0);
+                }
+                const int val = idx >= 0 ? (int)(word & 0xffffffffu) : 0;
+                const unsigned pm = __ballot_sync(FG_FULL_MASK, (word >> 62) == 2);
+                if (pm) {
+                    const int first = __ffs(pm) - 1;
+                    prefix += __reduce_add_sync(FG_FULL_MASK, lane <= first ? val : 0);
+                    break;
+                }
+                prefix += __reduce_add_sync(FG_FULL_MASK, val);
+                end -= 32;
+            }
+            if (lane == 0) atomicExch(&st[c], (2ull << 62) | (unsigned)(prefix + total));
+        }
+        if (lane == 0) {
+            s_pre = prefix;
+            s_tot = prefix + total;
+        }
     }
     __syncthreads();
     int64_t* mrow = a.m + i * a.n_maxuq;
     int64_t* nrow = a.m_not ? a.m_not + i * a.n_maxrs : nullptr;
-    const int pre = (int)s_pre;
+    const int pre = s_pre;
     const int cap_uq = (int)min(a.n_maxuq, (int64_t)INT32_MAX);
     const unsigned below = lanemask_lt();
 #pragma unroll
@@ -229,16 +238,12 @@ __global__ void __launch_bounds__(kThreads) k_oc_write(const MatArgs a) {
             nrow[o - r] = start + o;  // o - r non-members precede it
         }
     }
-    // -1 suffixes, shared by the object's blocks
-    const int64_t m_fill = min(s_tot, a.n_maxuq);
-    const int64_t stride = (int64_t)gridDim.x * kThreads;
-    for (int64_t x = m_fill + blockIdx.x * (int64_t)kThreads + threadIdx.x; x < a.n_maxuq; x += stride) mrow[x] = -1;
-    if (nrow) {
-        for (int64_t x = (len - s_tot) + blockIdx.x * (int64_t)kThreads + threadIdx.x; x < a.n_maxrs; x += stride)
-            nrow[x] = -1;
+    if (c == n_ch - 1) {  // -1 suffixes: this is the object's last chunk
+        const int64_t tot = s_tot;
+        for (int64_t x = min(tot, a.n_maxuq) + threadIdx.x; x < a.n_maxuq; x += kThreads) mrow[x] = -1;
+        if (nrow)
+            for (int64_t x = (len - tot) + threadIdx.x; x < a.n_maxrs; x += kThreads) nrow[x] = -1;
     }
-    __syncthreads();
-  }
 }
 
 }  // namespace oc
@@ -248,9 +253,9 @@ using namespace fg;
 using namespace fg::oc;
 
 namespace {
-uint64_t table_cap(int64_t n) {
+uint64_t table_cap(int64_t n) {  // load factor <= 0.8 even if every vertex is its own object
     uint64_t c = 1024;
-    while (c < 2 * (uint64_t)n) c <<= 1;
+    while (c < (uint64_t)n + (uint64_t)n / 4) c <<= 1;
     return c;
 }
 size_t n_scan_tiles(int64_t n) { return (size_t)ceil_div(n, (int64_t)kScanTile); }
@@ -330,7 +335,7 @@ extern "C" int fg_oc_matrices_workspace_size(int64_t n_unique, int64_t max_windo
     if (!bytes) return FG_ERR_NULL;
     if (n_unique < 0 || max_window < 0) return FG_ERR_BAD_SHAPE;
     const int64_t chunks = std::max<int64_t>(1, ceil_div(max_window, (int64_t)kChunk));
-    *bytes = align_up(sizeof(int32_t) * (size_t)(n_unique * chunks), 256) + 256;
+    *bytes = align_up(sizeof(unsigned long long) * (size_t)(n_unique * chunks), 256) + 256;
     return 0;
 }
 
@@ -358,13 +363,14 @@ extern "C" int fg_oc_matrices(const int64_t* asso, const int64_t* row_splits, in
     a.n_maxuq = n_maxuq;
     a.n_maxrs = n_maxrs;
     a.n_chunks = (int)std::max<int64_t>(1, ceil_div(std::min(max_window, n_maxrs), (int64_t)kChunk));
-    a.cnt = (int32_t*)workspace;
+    const size_t n_status = (size_t)n_unique * a.n_chunks;
+    a.status = (unsigned long long*)workspace;
+    a.ticket = (unsigned*)((char*)workspace + align_up(sizeof(unsigned long long) * n_status, 256));
     a.m = m;
     a.m_not = m_not;
     a.visits = (unsigned long long*)visits;
-    const dim3 grid((unsigned)a.n_chunks, (unsigned)std::min<int64_t>(n_unique, 65535));
-    k_oc_count<<<grid, kThreads, 0, st>>>(a);
-    FG_TRY(launched(st));
-    k_oc_write<<<grid, kThreads, 0, st>>>(a);
+    if (n_status > (size_t)INT32_MAX) return FG_ERR_BAD_SHAPE;
+    FG_CUDA(cudaMemsetAsync(workspace, 0, need, st));
+    k_oc_rows<<<(unsigned)n_status, kThreads, 0, st>>>(a);
     return launched(st);
 }
