@@ -15,7 +15,9 @@ max over ranks is reported.  Inputs are resident in HBM when the timed region
 starts; L2 is flushed (256 MiB write) before every step.  ``e2e`` repeats the
 measurement with pinned HOST buffers and the host<->device copies inside the
 timed region (copy streams overlap the compute: upstream gradients go in
-while the search runs, the neighbour matrix comes back while the backward runs).
+while the search runs, the neighbour matrix comes back while the backward runs),
+timed over steps run back to back like a training loop (``latency_ms_per_step``
+= one step alone, outputs on the host before the next starts).
 """
 
 from __future__ import annotations
@@ -362,7 +364,7 @@ def main():
         d_first = [torch.empty_like(h, device=dev) for h in h_first]
         d_late = [torch.empty_like(h, device=dev) for h in h_late]
 
-        def e2e_step(h_out=None):
+        def e2e_step(h_out=None, join=True):
             ev_first = torch.cuda.Event()
             ev_late = torch.cuda.Event()
             s_h2d.wait_stream(stream)
@@ -406,14 +408,17 @@ def main():
                         h_.copy_(o_, non_blocking=True)
                 for o_ in outs:  # the caching allocator must not recycle them early
                     o_.record_stream(s_d2h)
-                stream.wait_stream(s_d2h)
+                if join:
+                    stream.wait_stream(s_d2h)
             return outs
 
         outs = e2e_step()
         torch.cuda.synchronize()
         h_out = [torch.empty(o.shape, dtype=o.dtype).pin_memory() for o in outs]
-        t_e2e = 0.0
         e2e_steps = max(1, min(args.steps, 10))
+        # latency: each step on its own (its outputs back on the host before the
+        # next one starts)
+        t_lat = 0.0
         for it in range(e2e_steps + 1):
             if not args.no_flush:
                 flush.zero_()
@@ -424,13 +429,29 @@ def main():
             e1.record(stream)  # after stream.wait_stream(s_d2h): all copies done
             e1.synchronize()
             if it > 0:  # first iteration warms the pinned paths
-                t_e2e += e0.elapsed_time(e1)
-        e2e_ms = t_e2e / e2e_steps
+                t_lat += e0.elapsed_time(e1)
+        lat_ms = t_lat / e2e_steps
+        # throughput: the steps back to back, as a training loop runs them -- step
+        # i's outputs stream back while step i+1's inputs arrive and it computes
+        # (every step still copies all its inputs in and all its outputs out)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for it in range(e2e_steps):
+            if not args.no_flush:
+                flush.zero_()
+            e2e_step(h_out, join=False)
+        stream.wait_stream(s_d2h)
+        e1.record(stream)
+        e1.synchronize()
+        e2e_ms = e0.elapsed_time(e1) / e2e_steps
         h2d = sum(h.numel() * h.element_size() for h in h_first + h_late)
         d2h = sum(h.numel() * h.element_size() for h in h_out)
-        e2e = [e2e_ms, h2d, d2h]
+        e2e = [e2e_ms, h2d, d2h, lat_ms]
 
-    per_rank = [t_step / args.steps, n, e2e[0] if e2e else 0.0] + [t / args.steps for t in t_phase]
+    per_rank = [t_step / args.steps, n, e2e[0] if e2e else 0.0, e2e[3] if e2e else 0.0] + \
+        [t / args.steps for t in t_phase]
     allr = sharding.gather_floats(per_rank)
     if rank != 0:
         if world > 1:
@@ -439,7 +460,7 @@ def main():
         return 0
     ms = float(allr[:, 0].max())
     total_q = float(allr[:, 1].sum())
-    phase = {nm: float(allr[0, 3 + i]) for i, nm in enumerate(names)}
+    phase = {nm: float(allr[0, 4 + i]) for i, nm in enumerate(names)}
     value = total_q / (ms * 1e-3)
     peak, peak_src = load_peak()
     c_total = C_TOTAL[args.config]
@@ -486,7 +507,10 @@ def main():
         e2e_ms = float(allr[:, 2].max())
         line["e2e"] = {"value": total_q / (e2e_ms * 1e-3), "unit": "queries/s",
                        "h2d_bytes_per_step": int(e2e[1]), "d2h_bytes_per_step": int(e2e[2]),
-                       "ms_per_step": e2e_ms}
+                       "ms_per_step": e2e_ms,
+                       "mode": "steps back to back (step i's outputs copy back while step i+1's "
+                               "inputs arrive and it computes); every step moves all its bytes",
+                       "latency_ms_per_step": float(allr[:, 3].max())}
     if world == 1 and not args.no_cpu_baseline:
         try:
             tt, det = cpu_reference_step(coords_np, off_np, k, n_bins,
