@@ -776,13 +776,17 @@ __device__ __forceinline__ bool finish_query(WS& W, const TileArgs& a, int j, co
             bool tie = false;
             if (live) {
                 if (b1 - b0 <= 3) {  // the common case: unrolled, no loop
+                    // keys are >= 0: their bit patterns order like the floats, so
+                    // (key, position) compares as one 64-bit integer
+                    const unsigned kb = __float_as_uint(kk);
+                    const unsigned long long me = ((unsigned long long)kb << 32) | (unsigned)sl;
 #pragma unroll
                     for (int u = 0; u < 3; ++u) {
                         const int i = b0 + u;
-                        const float ki = W.skey[min(i, kCap - 1)];
-                        const bool mate = i < b1 && i != sl;
-                        r += (mate && (ki < kk || (ki == kk && i < sl))) ? 1 : 0;
-                        tie |= mate && ki == kk;
+                        const unsigned ib = __float_as_uint(W.skey[min(i, kCap - 1)]);
+                        const unsigned long long other = ((unsigned long long)ib << 32) | (unsigned)i;
+                        r += (i < b1 && other < me) ? 1 : 0;
+                        tie |= i < b1 && i != sl && ib == kb;
                     }
                 } else {
                     for (int i = b0; i < b1; ++i) {
