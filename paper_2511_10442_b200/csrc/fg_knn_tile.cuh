@@ -653,6 +653,9 @@ __device__ __forceinline__ void fused_gravnet(const TileArgs& a, const WS& W, in
 }
 
 constexpr int kRounds = (kCap + 31) / 32;
+#ifndef FG_FINISH_MATCH
+#define FG_FINISH_MATCH 0
+#endif
 
 // Global gathers of one query's list (coordinates and original ids of its
 // entries): issued for query j+1 while query j is being finished.
@@ -725,6 +728,7 @@ __device__ __forceinline__ bool finish_query(WS& W, const TileArgs& a, int j, co
     for (int t = 0; t < R; ++t) {
         bk[t] = key[t] < kInf ? bucket_of<DB>(key[t], inv_tau) : kBkt;
         idx[t] = 0;
+#if FG_FINISH_MATCH
         if (32 * t < m) {
             const unsigned mm = __match_any_sync(FG_FULL_MASK, bk[t]);
             const int leader = __ffs(mm) - 1;
@@ -733,6 +737,12 @@ __device__ __forceinline__ bool finish_query(WS& W, const TileArgs& a, int j, co
                 old = atomicAdd(&W.bcnt[bk[t]], (unsigned)__popc(mm));
             idx[t] = (int)__shfl_sync(FG_FULL_MASK, old, leader) + __popc(mm & lanemask_lt());
         }
+#else
+        // one shared-memory atomic per entry (native integer add; bucket mates
+        // in one warp instruction serialise, rare at ~0.45 entries per bucket);
+        // the in-bucket order this leaves is undone by the (key, position) rank
+        if (bk[t] < kBkt) idx[t] = (int)atomicAdd(&W.bcnt[bk[t]], 1u);
+#endif
     }
     __syncwarp();
     uint4 ca = *reinterpret_cast<const uint4*>(&W.bcnt[4 * lane]);
