@@ -1181,6 +1181,53 @@ __global__ void __launch_bounds__(kFinishWarps * 32, FG_FINISH_MINB) k_tile_fini
     const int need = a.k - 1;
     unsigned long long st_redo = 0;
     if (tiles_declined(a)) return;
+#ifndef FG_FINISH_PREFETCH
+#define FG_FINISH_PREFETCH 1
+#endif
+#if FG_FINISH_PREFETCH
+    // the next query's meta and list entries are loaded while this one is
+    // finished (the list row is read whole, without waiting for its length):
+    // only the coordinate / id gathers stay on the per-query critical path
+    const int64_t stride = (int64_t)gridDim.x * kFinishWarps;
+    int64_t p = blockIdx.x * (int64_t)kFinishWarps + (threadIdx.x >> 5);
+    float2 mt = p < n ? a.meta[p] : make_float2(0.f, -1.f);
+    int32_t lnext[kRounds];
+#pragma unroll
+    for (int t = 0; t < kRounds; ++t)
+        lnext[t] = (p < n && lane + 32 * t < kCap) ? a.lists[p * kCap + lane + 32 * t] : -1;
+    for (; p < n; p += stride) {
+        const int m = (int)mt.y;
+        const float tau_p = mt.x;
+        QLoads Q;
+        Q.m = m;
+#pragma unroll
+        for (int t = 0; t < kRounds; ++t) Q.cpos[t] = lnext[t];
+        const int64_t pn = p + stride;
+        mt = pn < n ? a.meta[pn] : make_float2(0.f, -1.f);
+#pragma unroll
+        for (int t = 0; t < kRounds; ++t)
+            lnext[t] = (pn < n && lane + 32 * t < kCap) ? a.lists[pn * kCap + lane + 32 * t] : -1;
+        if (m < 0) continue;  // already on the redo list
+#pragma unroll
+        for (int t = 0; t < kRounds; ++t) {
+            const int e = lane + 32 * t;
+            if (32 * t < m && e < m) {
+                Q.c[t] = a.sc[Q.cpos[t]];
+                Q.id[t] = a.sid[Q.cpos[t]];
+            } else {
+                Q.cpos[t] = -1;
+            }
+        }
+        const float4 q = a.sc[p];
+        const int32_t qid = a.sid[p];
+        const bool ok = finish_query<DB>(W, a, 0, Q, q, (int32_t)p, tau_p, qid, need);
+        if (!ok && lane == 0) {
+            a.redo[atomicAdd(&a.ctr[2], 1)] = (int32_t)p;
+            ++st_redo;
+        }
+        __syncwarp();
+    }
+#else
     for (int64_t p = blockIdx.x * (int64_t)kFinishWarps + (threadIdx.x >> 5); p < n;
          p += (int64_t)gridDim.x * kFinishWarps) {
         const float2 mt = a.meta[p];
@@ -1208,6 +1255,7 @@ __global__ void __launch_bounds__(kFinishWarps * 32, FG_FINISH_MINB) k_tile_fini
         }
         __syncwarp();
     }
+#endif
     if (a.stats && lane == 0 && st_redo) atomicAdd(&a.stats[TS_REDO], st_redo);
 }
 
