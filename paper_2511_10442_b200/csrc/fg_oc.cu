@@ -10,11 +10,13 @@
 // vertex order is exactly the reference's object order (splits ascending,
 // first occurrence inside a split).
 //
-// oc_helper: a 2-d grid of (window chunk, object) blocks.  Pass 1 counts each
-// chunk's members; pass 2 re-reads the chunk (L2-resident: every object of a
-// split scans the same window), places members at prefix + block-scan rank
-// (truncated to n_maxuq) and non-members at (offset in window) - (members
-// before it), and fills the -1 suffixes.  Integer work throughout: bit-exact.
+// oc_helper: one block per (object, 2048-vertex window chunk), in ticket
+// order.  Members of the chunk are ranked by ballots; the members before the
+// chunk come from a decoupled look-back over the object's earlier chunks;
+// members go to m[i, rank] (truncated to n_maxuq), non-members to
+// m_not[i, offset - rank]; the object's last chunk fills the -1 suffixes.  The
+// windows are re-read per object from L2 (every object of a split scans the
+// same window).  Integer work throughout: bit-exact.
 #include "fg_common.cuh"
 #include "fg_scan.cuh"
 
