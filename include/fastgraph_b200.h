@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define FG_ABI_VERSION 2
+#define FG_ABI_VERSION 3
 
 enum fg_status {
     FG_OK = 0,
@@ -48,7 +48,8 @@ enum fg_status {
     FG_ERR_NULL = -5,           /* required pointer is NULL                             */
     FG_ERR_TOO_MANY_DIMS = -6,  /* n_coords > 16                                        */
     FG_ERR_BAD_RADIUS = -7,     /* max_radius2 < 0 (G/knn.py:57-58 BadKError)          */
-    FG_ERR_BAD_CAPACITY = -8    /* n_maxuq / n_maxrs < 1 (G/ocgraph.py:176-179)         */
+    FG_ERR_BAD_CAPACITY = -8,   /* n_maxuq / n_maxrs < 1 (G/ocgraph.py:176-179)         */
+    FG_ERR_UNSUPPORTED = -9     /* sizes outside the requested mode's limits            */
 };
 
 /* Option bits for fg_knn_fwd (mirror KnnOptions, G/knn.py:34-45, and the
@@ -137,17 +138,29 @@ int fg_knn_stats(uint64_t *out, int32_t n, int32_t reset);
 
 /* ---------------------------------------------------------------- backward */
 
-int fg_knn_bwd_workspace_size(int64_t n, int32_t n_coords, size_t *bytes);
+int fg_knn_bwd_workspace_size(int64_t n, int32_t n_coords, int32_t k, size_t *bytes);
 
 /* binned_select_knn backward.  Replaces knn_backward (G/knn.py:135-168):
  * for every valid non-self slot (v,s) -> u with upstream g = grad_d2[v,s],
  * grad[v] += 2g(x_v - x_u) and grad[u] -= 2g(x_v - x_u).  Terms are formed
- * exactly in float64 and accumulated to float64-class precision (compensated
- * fp32x4 atomics, error ~2^-48 of the term magnitudes); grad_coords is float32
- * (or double with grad_is_f64).  `order` (nullable) is the row visiting order,
- * e.g. the sort_order of fg_bin_by_coordinates (spatial locality). */
+ * exactly in float64 (fp32 g and x).  Two accumulation paths:
+ *  - default: compensated fp32x4 atomics (hi + exact TwoSum error), ~2^-48 of
+ *    the term magnitudes, fastest, not bitwise repeatable;
+ *  - FG_BWD_DETERMINISTIC (up to 2^23 vertices and 2^32 slots): the slots are
+ *    transposed into 512-position destination buckets (counting sorts, no
+ *    floating-point atomics) and every destination sums its terms as int64
+ *    fixed point (order-independent), ~2^-42 of the bucket's largest term:
+ *    bitwise repeatable run to run like the reference's fixed-order np.add.at
+ *    (pkg/tests/test_knn.py:302-309).
+ * grad_d2 is float32 (a float64 upstream is rounded to float32 by the torch
+ * op).  grad_coords is float32 (or double with FG_BWD_F64).  `order`
+ * (nullable) is the row visiting order, e.g. the sort_order of
+ * fg_bin_by_coordinates (spatial locality).
+ * Workspace from fg_knn_bwd_workspace_size(n, n_coords, k). */
+#define FG_BWD_F64 0x1
+#define FG_BWD_DETERMINISTIC 0x2
 int fg_knn_bwd(const float *coords, int64_t n, int32_t n_coords, const int32_t *idx, int32_t k,
-               const float *grad_d2, const int32_t *order, void *grad_coords, int32_t grad_is_f64,
+               const float *grad_d2, const int32_t *order, void *grad_coords, int32_t grad_flags,
                void *workspace, size_t workspace_bytes, void *stream);
 
 /* ---------------------------------------------------------------- GravNet */

@@ -25,6 +25,8 @@ FG_KNN_STATS = 0x100
 FG_KNN_NO_TILE = 0x200
 FG_KNN_FUSED_GN = 0x400
 FG_KNN_FUSED_EPI = 0x800
+FG_BWD_F64 = 0x1
+FG_BWD_DETERMINISTIC = 0x2
 FG_REDUCE_MEAN = 0
 FG_REDUCE_MAX = 1
 
@@ -58,7 +60,7 @@ _SIGS = {
     "fg_knn_gravnet_fwd_ws": ([_P, _P, _P, _P, _P, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32,
                                _U32, _P, _I32, _D, _P, _I32, _I32, _P, _P, _P, _P,
                                ctypes.c_size_t, _P], ctypes.c_int),
-    "fg_knn_bwd_workspace_size": ([_I64, _I32, _SZ], ctypes.c_int),
+    "fg_knn_bwd_workspace_size": ([_I64, _I32, _I32, _SZ], ctypes.c_int),
     "fg_knn_bwd": ([_P, _I64, _I32, _P, _I32, _P, _P, _P, _I32, _P, ctypes.c_size_t, _P],
                    ctypes.c_int),
     "fg_gravnet_fwd": ([_P, _I64, _I32, _P, _P, _I32, _D, _P, _I32, _I32, _P, _P, _P],
@@ -113,7 +115,7 @@ def check(rc: int, what: str = "") -> None:
         raise BadKError(msg)
     if rc == -3:
         raise TooFewDimsError(msg)
-    if rc in (-2, -6):
+    if rc in (-2, -6, -9):
         raise BadShapeError(msg)
     if rc == -4:
         raise ShapeMismatchError(msg)

@@ -473,6 +473,7 @@ extern "C" const char* fg_error_string(int code) {
         case FG_ERR_TOO_MANY_DIMS: return "n_coords must be <= 16";
         case FG_ERR_BAD_RADIUS: return "max_radius2 must be >= 0";
         case FG_ERR_BAD_CAPACITY: return "capacities must be >= 1";
+        case FG_ERR_UNSUPPORTED: return "sizes outside the limits of the requested mode (deterministic backward: n <= 2^23, n*k < 2^32)";
         default: return code > 0 ? cudaGetErrorString((cudaError_t)code) : "unknown error";
     }
 }

@@ -96,7 +96,10 @@ def brute_force_knn(cloud: PointCloud, opts: KnnOptions, *, d2_f64: bool = False
 
 
 def knn_backward(cloud: PointCloud, neighbors: NeighborMatrix, upstream) -> torch.Tensor:
-    """G/knn.py:135-168: d(sum g*d2)/d coords; float64 terms and sums."""
+    """G/knn.py:135-168: d(sum g*d2)/d coords.  Terms exact in float64, the
+    upstream rounded to float32; bitwise repeatable like the reference's
+    fixed-order accumulation (the deterministic transposed kernel) up to 2^23
+    vertices, the atomic kernel above that."""
     up = upstream if isinstance(upstream, torch.Tensor) else torch.as_tensor(upstream)
     up = up.to(cloud.coords.device)
     if tuple(up.shape) != tuple(neighbors.dist2.shape):
@@ -105,7 +108,9 @@ def knn_backward(cloud: PointCloud, neighbors: NeighborMatrix, upstream) -> torc
     if neighbors.n_vertices != cloud.n_vertices:
         raise ShapeMismatchError(f"neighbours cover {neighbors.n_vertices} vertices, "
                                  f"cloud has {cloud.n_vertices}")
-    return ops.binned_select_knn_grad(up, neighbors.indices, cloud.coords.detach())
+    n, k = neighbors.indices.shape
+    det = n <= (1 << 23) and n * k < (1 << 32)
+    return ops.binned_select_knn_grad(up, neighbors.indices, cloud.coords.detach(), None, det)
 
 
 def knn_with_grad(cloud: PointCloud, index: BinIndex, opts: KnnOptions):

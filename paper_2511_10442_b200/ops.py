@@ -196,7 +196,7 @@ def _knn_fake(coords, row_splits, bin_idx, sort_order, bin_bounds, dim_mins, wid
 
 @torch.library.custom_op(f"{_LIB_NS}::binned_select_knn_grad", mutates_args=())
 def binned_select_knn_grad(grad_d2: Tensor, idx: Tensor, coords: Tensor,
-                           order: Optional[Tensor] = None) -> Tensor:
+                           order: Optional[Tensor] = None, deterministic: bool = False) -> Tensor:
     _require_cuda(grad_d2, idx, coords)
     L = _lib.load()
     n, n_c = coords.shape
@@ -212,15 +212,16 @@ def binned_select_knn_grad(grad_d2: Tensor, idx: Tensor, coords: Tensor,
     out_f64 = coords.dtype == torch.float64
     grad = torch.empty((n, n_c), dtype=torch.float64 if out_f64 else torch.float32,
                        device=coords.device)
-    ws = _ws(_lib.size_out(L.fg_knn_bwd_workspace_size, n, n_c), coords.device)
+    ws = _ws(_lib.size_out(L.fg_knn_bwd_workspace_size, n, n_c, k), coords.device)
     od = _order(order, n, coords.device)
-    _lib.check(L.fg_knn_bwd(_p(c), n, n_c, _p(ix), k, _p(g), _p(od), _p(grad), int(out_f64),
+    flags = (_lib.FG_BWD_F64 if out_f64 else 0) | (_lib.FG_BWD_DETERMINISTIC if deterministic else 0)
+    _lib.check(L.fg_knn_bwd(_p(c), n, n_c, _p(ix), k, _p(g), _p(od), _p(grad), flags,
                             _p(ws), ws.numel(), _stream(c)), "binned_select_knn_grad")
     return grad
 
 
 @binned_select_knn_grad.register_fake
-def _knn_grad_fake(grad_d2, idx, coords, order=None):
+def _knn_grad_fake(grad_d2, idx, coords, order=None, deterministic=False):
     return torch.empty_like(coords)
 
 

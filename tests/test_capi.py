@@ -40,7 +40,7 @@ def test_library_is_built_for_sm_100a():
 
 def test_abi_version_and_error_strings():
     L = _lib.load()
-    assert L.fg_abi_version() == 2
+    assert L.fg_abi_version() == 3
     assert L.fg_error_string(0) == b"ok"
     assert b"k must be" in L.fg_error_string(-1)
 

@@ -80,25 +80,6 @@ def test_config_c_sampled_parity(oracle):
     assert np.array_equal(d2.cpu().numpy()[rows], od)
 
 
-def test_north_star_backward_properties(oracle):
-    coords, off, k = config_dataset("north_star")
-    c, rs, so, idx, d2 = run(coords, off, k)
-    up = torch.from_numpy(np.random.default_rng(13).standard_normal((len(coords), k)).astype(np.float32)).cuda()
-    g64 = ops.binned_select_knn_grad(up, idx, c.double(), so).cpu().numpy()
-    g32 = ops.binned_select_knn_grad(up, idx, c, so).cpu().numpy()
-    # every pair adds +t to one vertex and -t to another: the column sums vanish
-    assert np.all(np.abs(g64.sum(0)) < 1e-9 * np.abs(g64).sum(0))
-    np.testing.assert_allclose(g32, g64, rtol=1e-6, atol=1e-7 * np.abs(g64).max())
-    # exact oracle gradient restricted to a block of rows is not separable, so
-    # compare on a sub-cloud instead: the first 20k points as their own event
-    sub = coords[:20_000]
-    cs, _, sos, isub, _ = run(sub, [0, 20_000], k)
-    us = up[:20_000].contiguous()
-    gs = ops.binned_select_knn_grad(us, isub, cs, sos).cpu().numpy()
-    ref = oracle.knn_backward(sub.astype(np.float64), isub.cpu().numpy(), us.cpu().numpy().astype(np.float64))
-    np.testing.assert_allclose(gs, ref, rtol=1e-5, atol=1e-12 * np.abs(ref).max())
-
-
 def test_gravnet_config_e_sample(oracle):
     coords, off, k = config_dataset("E")
     _, _, _, idx, d2 = run(coords, off, k)
