@@ -3,21 +3,25 @@
 backward (BASELINE.json metric: N=1M, d=4, k=40, fwd+bwd; % of HBM roofline).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config north_star|A|B|C|D|E]
-    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N   (N > 1)
     python bench.py --impl reference     (the reference's own CPU path, rank 0)
+
+``--gpus N > 1`` without a torchrun environment re-launches this script under
+``torch.distributed.run`` with N ranks (one per GPU, NCCL, 127.0.0.1).
 
 Workload (default ``north_star``): one step = one pass of the path over one
 event of 1,000,000 uniform points in [0,1)^4 (the reference's generator,
 seed 3 + rank, cast to float32), k = 40, fixed upstream gradient for the
 backward.  Multi-GPU = event sharding by row splits, one event per GPU (weak
-scaling), no collective in the data path; timings are all-gathered and the
-max over ranks is reported.  Inputs are resident in HBM when the timed region
-starts; L2 is flushed (256 MiB write) before every step.  ``e2e`` repeats the
-measurement with pinned HOST buffers and the host<->device copies inside the
-timed region (copy streams overlap the compute: upstream gradients go in
-while the search runs, the neighbour matrix comes back while the backward runs),
-timed over steps run back to back like a training loop (``latency_ms_per_step``
-= one step alone, outputs on the host before the next starts).
+scaling, ``value`` = all ranks' queries / max-over-ranks step time), no
+collective in the data path.  Every run also reports ``strong_scaling``: the
+64-event batch of config D sharded by row splits over the N ranks (global
+n_bins, global neighbour ids), T_N (max over ranks) against T_1 (the whole
+batch on rank 0's GPU alone) on the same batch.
+
+Inputs are resident in HBM when the timed region starts; L2 is flushed (256 MiB
+write) before every step.  ``e2e`` repeats the measurement with pinned HOST
+buffers and the host<->device copies inside the timed region, steps back to
+back like a training loop (``latency_ms_per_step`` = one step alone).
 """
 
 from __future__ import annotations
@@ -25,6 +29,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -42,9 +47,16 @@ METRIC = "binned kNN graph-build ms & queries/s, N=1M d=4 k=40, fwd+bwd; % HBM r
 C_TOTAL = {"A": 8.6e5, "B": 3.68e9, "north_star": 7.47e8, "C": 1.81e11, "D": 4.51e9,
            "E": 3.31e8}
 
+# query sample per reference step (DirectionMask: sample rows are queries, every
+# vertex stays a candidate, so the per-query cost is the full problem's)
+REF_QUERY_FRAC = {"north_star": 1.0, "A": 1.0, "B": 1.0, "C": 0.002, "D": 0.1, "E": 1.0}
 
-# query sample for the CPU reference where its full search would take minutes+
-REF_QUERY_FRAC = {"C": 0.002, "D": 0.1}
+SEARCH_KERNELS = ("k_tiles", "k_tile_search", "k_tile_finish", "k_knn_fwd")
+
+DESC = {"north_star": "north_star: 1 event x 1,000,000 uniform points per GPU, d=4, k=40",
+        "A": "A: 10k points d=3 k=16", "B": "B: 200k clustered points d=4 k=40",
+        "C": "C: 1M points d=10 k=64", "E": "E: 500k points d=4 k=40 + GravNet (F=64)",
+        "D": "D: 64 events x 100k points d=4 k=40, row splits sharded over the ranks"}
 
 
 def algorithmic_bytes(n, d, k, c_total):
@@ -63,11 +75,8 @@ def load_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-SEARCH_KERNELS = ("k_tiles", "k_tile_search", "k_tile_finish", "k_knn_fwd")
-
-
 def load_traffic(config):
-    """dram bytes per search call (its kernels) from the committed ncu captures."""
+    """DRAM bytes per search call (its kernels) from the committed ncu captures."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as fh:
@@ -79,29 +88,56 @@ def load_traffic(config):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled while the timed loop runs."""
+    """SM clocks + throttle reasons sampled through NVML every millisecond while
+    the timed loop runs (nvidia-smi fallback)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
-        self.samples = []
+        self.sm, self.mx, self.reasons = [], [], set()
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+            self._nvml = pynvml
+        except Exception:
+            self._nvml = None
+
+    def _sample(self):
+        if self._nvml is not None:
+            p = self._nvml
+            self.sm.append(float(p.nvmlDeviceGetClockInfo(self._h, p.NVML_CLOCK_SM)))
+            self.mx.append(float(p.nvmlDeviceGetMaxClockInfo(self._h, p.NVML_CLOCK_SM)))
+            r = p.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            for name, const in self.REASONS:
+                if r & getattr(p, const):
+                    self.reasons.add(name)
+            return
+        out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,"
+                              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip().split(",")
+        self.sm.append(float(out[0]))
+        self.mx.append(float(out[1]))
+        for i, (name, _) in enumerate(self.REASONS):
+            if out[2 + i].strip().lower().startswith("active"):
+                self.reasons.add(name)
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.FIELDS,
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                self._sample()
             except Exception:
                 return
-            self._stop.wait(0.05)
+            self._stop.wait(0.001)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -114,49 +150,48 @@ class ClockSampler:
             self._t.join(timeout=10)
 
     def summary(self):
-        if not self.samples:
+        if not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 2 + i and s[2 + i].lower().startswith("active")})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+        return {"sm_mhz": float(np.median(self.sm)), "sm_max_mhz": max(self.mx),
+                "reasons": sorted(self.reasons), "samples": len(self.sm),
+                "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
 def workload(config, rank, world):
+    """-> (coords f32 (local rows), local row splits, k, n_bins, scaling, desc)."""
     from paper_2511_10442_b200.datasets import CONFIGS, generate_dataset
     n, d, splits, k, dist, seed = CONFIGS[config]
-    if config == "D":
-        # strong scaling: the 64-event batch is sharded by row splits
+    if config == "D":  # strong scaling: the 64-event batch is sharded by row splits
         from paper_2511_10442_b200 import sharding
         coords, off = generate_dataset(n, d, splits, seed, dist)
         sh = sharding.shard(off, rank, world)
         n_bins = sharding.global_n_bins(off, k, d)
         c = coords[sh.vertex_lo:sh.vertex_hi].astype(np.float32)
-        return c, sh.local_offsets, k, n_bins, "strong", \
-            f"D: 64 events x 100k points (events {sh.event_lo}..{sh.event_hi - 1} on rank {rank})"
-    # weak scaling: one event per GPU
+        return c, sh.local_offsets, k, n_bins, "strong", DESC["D"]
     coords, off = generate_dataset(n, d, splits, seed + rank, dist)
     from paper_2511_10442_b200.binning import compute_n_bins, default_bin_dims
     n_bins = compute_n_bins(int(np.diff(off).max()), k, default_bin_dims(d))
-    desc = {"north_star": "north_star: 1 event x 1,000,000 uniform points per GPU, d=4, k=40",
-            "A": "A: 10k points d=3 k=16", "B": "B: 200k clustered points d=4 k=40",
-            "C": "C: 1M points d=10 k=64", "E": "E: 500k points d=4 k=40"}[config]
-    return coords.astype(np.float32), off, k, n_bins, "weak", desc
+    return coords.astype(np.float32), off, k, n_bins, "weak", DESC[config]
 
 
-def cpu_reference_step(coords32, offsets, k, n_bins, bwd_rows=100_000, seed=0,
-                       query_frac=1.0):
-    """One step of the reference's own CPU path on this host: build_index +
-    binned_knn over ALL queries (oracle/_ref = the reference's compiled
-    _binned_cy kernels, all host threads) + knn_backward (the oracle's
-    restatement of the reference's numpy np.add.at code, 1 core) on a sample of
-    rows, extrapolated linearly (the backward has no per-call fixed cost).
-    Returns (seconds for the full workload, details)."""
-    from oracle import oracle as O  # cpu_baseline leg only
+def config_keys(config, n, d, k, n_bins, events, flushed):
+    """The workload description shared by both arms (same keys)."""
+    return {"workload": DESC[config], "n_points_per_gpu": n, "d": d, "k": k, "n_bins": n_bins,
+            "d_bin": min(d, 5), "events": events,
+            "l2": "flushed (256 MiB write) before every step" if flushed else "no flush"}
+
+
+def cpu_reference_step(coords32, offsets, k, n_bins, query_frac=1.0, bwd_rows=100_000, seed=0):
+    """One step of the reference's own CPU path on this host: build_index over
+    the whole event + binned_knn over all queries (or, where the full search
+    takes minutes, a DirectionMask query sample: sample = role 3, the rest stay
+    candidates with role 0, so the per-query work is the full problem's) on all
+    host threads (oracle/_ref = the reference's compiled _binned_cy kernels),
+    then the reference's numpy knn_backward (np.add.at, 1 core) over a random
+    sample of bwd_rows rows.  Returns (seconds, queries/s, details): the rate is
+    1 / (fwd s per query + bwd s per row), both measured in this step -- no time
+    is extrapolated."""
+    from oracle import oracle as O  # cpu_baseline / reference leg only
     ref = O.load_ref_kernels()
     kind = "reference" if ref is not None else "port"
     c64 = coords32.astype(np.float64)
@@ -164,46 +199,39 @@ def cpu_reference_step(coords32, offsets, k, n_bins, bwd_rows=100_000, seed=0,
     d_bin = min(n_c, 5)
     threads = os.cpu_count() or 1
     rng = np.random.default_rng(seed)
-    mask = None
-    if query_frac < 1.0:  # configs whose full CPU search takes hours (C): query sample
-        mask = np.zeros(n, np.int8)  # role 0: candidate only
-        mask[rng.choice(n, size=max(1, int(n * query_frac)), replace=False)] = 3
-
-    def run(m):
-        t0 = time.perf_counter()
-        if ref is not None:
-            bi, so, bb, mins, widths = ref.build_index(c64, offsets, d_bin, n_bins)
-            oi = np.empty((n, k), np.int32)
-            od = np.empty((n, k), np.float64)
-            ref.binned_knn(c64, bi, so, bb, np.full(d_bin, n_bins, np.int64),
-                           widths.min(axis=1).copy(), np.zeros(1, np.int8) if m is None else m,
-                           m is not None, 0.0, False, False, k, oi, od, threads)
-        else:
-            oi, od = O.knn_refslot(c64, offsets, k, n_bins=n_bins, dir_mask=m, threads=threads)
-        return time.perf_counter() - t0, oi
-
-    if mask is None:
-        t_fwd, out_i = run(None)
-    else:  # fixed per-vertex cost measured with zero queries, query cost scaled
-        t_zero, _ = run(np.zeros(n, np.int8))
-        t_s, out_i = run(mask)
-        t_fwd = t_zero + max(t_s - t_zero, 0.0) / query_frac
-        sel = np.nonzero(mask == 3)[0]
-        out_i = out_i.copy()
-        out_i[np.setdiff1d(np.arange(n), sel)] = out_i[sel[0]]  # bwd rows use real neighbours
-    rows = rng.choice(n, size=min(bwd_rows, n), replace=False)
-    up = rng.standard_normal((len(rows), k))
+    if query_frac < 1.0:
+        q_rows = np.sort(rng.choice(n, size=max(1, int(n * query_frac)), replace=False))
+        mask = np.zeros(n, np.int8)
+        mask[q_rows] = 3
+    else:
+        q_rows, mask = np.arange(n), None
     t0 = time.perf_counter()
-    O.knn_backward_numpy(c64, out_i[rows], up, rows)
-    t_bwd = (time.perf_counter() - t0) * (n / len(rows))
-    total = t_fwd + t_bwd
-    return total, {"kind": kind, "cores": threads, "t_fwd_s": t_fwd, "t_bwd_s": t_bwd,
-                   "sample": (f"fwd: build_index + binned_knn over "
-                              + (f"all {n} queries" if mask is None else
-                                 f"a {query_frac:.0%} query sample (fixed per-vertex cost timed "
-                                 f"separately, query cost x{1 / query_frac:.0f})")
-                              + f" (reference compiled _binned_cy, {threads} threads); bwd: numpy "
-                              f"knn_backward on {len(rows)} rows x{n / len(rows):.0f} (1 core)")}
+    if ref is not None:
+        bi, so, bb, mins, widths = ref.build_index(c64, offsets, d_bin, n_bins)
+        oi = np.empty((n, k), np.int32)
+        od = np.empty((n, k), np.float64)
+        ref.binned_knn(c64, bi, so, bb, np.full(d_bin, n_bins, np.int64), widths.min(axis=1).copy(),
+                       np.zeros(1, np.int8) if mask is None else mask, mask is not None, 0.0, False,
+                       False, k, oi, od, threads)
+    else:
+        oi, od = O.knn_refslot(c64, offsets, k, n_bins=n_bins, dir_mask=mask, threads=threads)
+    t_fwd = time.perf_counter() - t0
+    rows = np.sort(rng.choice(q_rows, size=min(bwd_rows, len(q_rows)), replace=False))
+    up = rng.standard_normal((len(rows), k))
+    t1 = time.perf_counter()
+    O.knn_backward_numpy(c64, oi[rows], up, rows)
+    t_bwd = time.perf_counter() - t1
+    rate = 1.0 / (t_fwd / len(q_rows) + t_bwd / len(rows))
+    sample = (f"fwd: build_index over all {n} points + binned_knn over "
+              + (f"all {n} queries" if mask is None else
+                 f"{len(q_rows)} sampled queries (DirectionMask: sample = role 3, rest = role 0 "
+                 "candidates)")
+              + f" (reference compiled _binned_cy, {threads} threads); bwd: numpy knn_backward "
+              f"(np.add.at, 1 core) over {len(rows)} sampled rows; rate = 1 / (fwd s/query + "
+              "bwd s/row), both measured in the step")
+    return t_fwd + t_bwd, rate, {"kind": kind, "cores": threads, "t_fwd_s": t_fwd,
+                                 "t_bwd_s": t_bwd, "fwd_queries": int(len(q_rows)),
+                                 "bwd_rows": int(len(rows)), "sample": sample}
 
 
 def run_reference(args):
@@ -211,27 +239,139 @@ def run_reference(args):
     if rank != 0:
         return 0
     coords, off, k, n_bins, scaling, desc = workload(args.config, 0, 1)
-    n = coords.shape[0]
-    times = []
-    det = None
+    n, d = coords.shape
+    frac = REF_QUERY_FRAC.get(args.config, 1.0)
+    times, fwd_t, bwd_t, det = [], [], [], None
     for s_ in range(max(args.warmup, 0) + args.steps):
-        tt, det = cpu_reference_step(coords, off, k, n_bins, seed=100 + s_,
-                                     query_frac=REF_QUERY_FRAC.get(args.config, 1.0))
+        tt, rate, det = cpu_reference_step(coords, off, k, n_bins, frac, seed=100 + s_)
         if s_ >= args.warmup:
             times.append(tt)
-    t = float(np.mean(times))
-    value = n / t
+            fwd_t.append(det["t_fwd_s"] / det["fwd_queries"])
+            bwd_t.append(det["t_bwd_s"] / det["bwd_rows"])
+    value = 1.0 / (float(np.mean(fwd_t)) + float(np.mean(bwd_t)))
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": scaling,
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": desc, "n_points": n, "k": k, "n_bins": n_bins},
+            "ms_per_step": float(np.mean(times)) * 1e3, "higher_is_better": True,
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference generate_dataset)",
+            "config": config_keys(args.config, n, d, k, n_bins, len(off) - 1, False),
+            "per_step": {"fwd_queries": det["fwd_queries"], "bwd_rows": det["bwd_rows"],
+                         "us_per_query_fwd": float(np.mean(fwd_t)) * 1e6,
+                         "us_per_row_bwd": float(np.mean(bwd_t)) * 1e6},
             "cpu_baseline": {"value": value, "unit": "queries/s", "cores": det["cores"],
                              "kind": det["kind"], "sample": det["sample"]},
             "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn(args):
+    """--gpus N > 1 outside torchrun: re-launch under torch.distributed.run."""
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible", file=sys.stderr)
+        return 2
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+           str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
+def timed_steps(step, n_steps, warmup, stream, flush=None, world=1):
+    """Warm-up, then n_steps steps bracketed by barrier + synchronize, each timed
+    with CUDA events on ``stream``; returns (mean ms per step, phase ms list)."""
+    import torch
+    import torch.distributed as dist
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    tot, phases = 0.0, None
+    for _ in range(n_steps):
+        if flush is not None:
+            flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        marks = step()
+        e1.record(stream)
+        e1.synchronize()
+        tot += e0.elapsed_time(e1)
+        if marks:
+            m = [e0] + marks + [e1]
+            ph = [m[i].elapsed_time(m[i + 1]) for i in range(len(m) - 1)]
+            phases = ph if phases is None else [a + b for a, b in zip(phases, ph)]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    return tot / n_steps, [p / n_steps for p in phases] if phases else []
+
+
+def strong_scaling(args, rank, world, dev, flush):
+    """Config D (64 events x 100k, d=4, k=40) sharded by row splits: T_N = max
+    over ranks of one step of the rank's share; T_1 = the whole batch on rank 0's
+    GPU alone.  Same batch, same global n_bins, global neighbour ids."""
+    import torch
+    import torch.distributed as dist
+    from paper_2511_10442_b200 import ops, sharding
+    from paper_2511_10442_b200.datasets import CONFIGS, generate_dataset
+    n, d, splits, k, distn, seed = CONFIGS["D"]
+    coords, off = generate_dataset(n, d, splits, seed, distn)
+    coords = coords.astype(np.float32)
+    nb = sharding.global_n_bins(off, k, d)
+    stream = torch.cuda.current_stream(dev)
+    steps = max(1, min(args.steps, 5))
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(77)
+
+    def make_step(lo, hi, offs):
+        c = torch.from_numpy(coords[lo:hi]).to(dev)
+        rs = torch.from_numpy(np.asarray(offs, np.int64)).to(dev)
+        up = torch.randn((hi - lo, k), generator=gen, device=dev)
+
+        def step():
+            bi, so, bb, mins, widths, sc = ops.bin_by_coordinates(c, rs, min(d, 5), nb)
+            idx, d2 = ops.binned_select_knn(c, rs, bi, so, bb, mins, widths, sc, k, min(d, 5), nb,
+                                            None, None, False, False)
+            ops.binned_select_knn_grad(up, idx, c, so)
+            return []
+        return step
+
+    sh = sharding.shard(off, rank, world)
+    t_n, _ = timed_steps(make_step(sh.vertex_lo, sh.vertex_hi, sh.local_offsets), steps, 2, stream,
+                         flush, world)
+    t_all = sharding.gather_floats([t_n, float(sh.n_events)])
+    t1 = None
+    if world == 1:
+        t1 = t_n
+    else:
+        if rank == 0:
+            t1, _ = timed_steps(make_step(0, n, off), steps, 2, stream, flush, 1)
+        dist.barrier()
+    if rank != 0:
+        return None
+    tn = float(t_all[:, 0].max())
+    return {"workload": "D: 64 events x 100,000 uniform points, d=4, k=40, fwd+bwd; row splits "
+                        "sharded over the ranks (contiguous event ranges), global n_bins, no "
+                        "collective in the data path",
+            "n_gpus": world, "steps": steps, "t1_ms": t1, "tn_ms": tn,
+            "speedup_t1_over_tn": t1 / tn, "events_per_rank": [int(x) for x in t_all[:, 1]],
+            "t_rank_ms": [float(x) for x in t_all[:, 0]],
+            "note": "T_1 = the whole batch on rank 0's GPU alone (same process, same batch)"}
 
 
 def main():
@@ -244,9 +384,14 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--no-strong", action="store_true", help="skip the config-D strong-scaling block")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="bitwise-repeatable backward (FG_BWD_DETERMINISTIC)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn(args)
 
     import torch
     import torch.distributed as dist
@@ -259,7 +404,6 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
 
-    import paper_2511_10442_b200 as fg
     from paper_2511_10442_b200 import _lib, ops, sharding
     _lib.load()
 
@@ -271,8 +415,9 @@ def main():
     coords = torch.from_numpy(coords_np).to(dev)
     rs = torch.from_numpy(off_np).to(dev)
     up = torch.from_numpy(up_np).to(dev)
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    flush = None if args.no_flush else torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
+    det = args.deterministic
 
     gravnet = args.config == "E"  # config E: the GravNetOp layer on top of the search
     if gravnet:
@@ -280,71 +425,50 @@ def main():
         feats = torch.from_numpy(rng.standard_normal((n, n_feat)).astype(np.float32)).to(dev)
         up_agg = torch.from_numpy(rng.standard_normal((n, 2 * n_feat)).astype(np.float32)).to(dev)
 
-    def step(c, u, f=None, ua=None):
-        """One pass of the path; returns outputs and the phase events."""
-        evs = []
-
+    def run_path(c, u, f=None, ua=None, marks=None):
+        """One pass of the path; ``marks`` collects phase events."""
         def mark():
-            e = torch.cuda.Event(enable_timing=True)
-            e.record(stream)
-            evs.append(e)
+            if marks is not None:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(stream)
+                marks.append(e)
 
         bi, so, bb, mins, widths, sc = ops.bin_by_coordinates(c, rs, d_bin, n_bins)
         mark()
-        if gravnet:  # GravNetOp layer: the fused search + aggregation, then its backward
+        if gravnet:  # GravNetOp layer: search + aggregation, then its backward
             idx, d2, agg = ops.knn_gravnet(c, rs, bi, so, bb, mins, widths, sc, k, d_bin, n_bins,
                                            f, 10.0, [0, 1], True)
             mark()
             gf, gd = ops.gravnet_aggregate_grad(ua, f, idx, d2, 10.0, [0, 1], True, so)
             mark()
-            g = ops.binned_select_knn_grad(gd, idx, c, so)
-            return (idx, d2, g, agg, gf), evs
+            g = ops.binned_select_knn_grad(gd, idx, c, so, det)
+            return [idx, d2, agg], [g, gf]
         idx, d2 = ops.binned_select_knn(c, rs, bi, so, bb, mins, widths, sc, k, d_bin, n_bins,
                                         None, None, False, False)
         mark()
-        g = ops.binned_select_knn_grad(u, idx, c, so)
-        return (idx, d2, g), evs
+        g = ops.binned_select_knn_grad(u, idx, c, so, det)
+        return [idx, d2], [g]
 
-    # warm-up: at least W steps and at least 1.5 s of work, so the SM clocks have
-    # left their idle state before anything is timed
+    names = (["bin_by_coordinates", "knn_gravnet_fwd", "gravnet_bwd", "knn_bwd"] if gravnet
+             else ["bin_by_coordinates", "knn_fwd", "knn_bwd"])
+
+    def step():
+        marks = []
+        run_path(coords, up, feats if gravnet else None, up_agg if gravnet else None, marks)
+        return marks
+
+    # warm-up: at least W (>= 3) steps and 1.5 s of work, so the SM clocks have left idle
     t_warm = time.perf_counter()
     it = 0
     while it < max(args.warmup, 3) or time.perf_counter() - t_warm < 1.5:
-        step(coords, up, feats if gravnet else None, up_agg if gravnet else None)
+        step()
         torch.cuda.synchronize()
         it += 1
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-
-    sampler = ClockSampler(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[0])
-                           if os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")[0].isdigit()
-                           else local)
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")[local:local + 1]
+    sampler = ClockSampler(int(vis[0]) if vis and vis[0].isdigit() else local)
     launches0 = _lib.launch_count()
-    names = (["bin_by_coordinates", "knn_gravnet_fwd", "gravnet_bwd", "knn_bwd"] if gravnet
-             else ["bin_by_coordinates", "knn_fwd", "knn_bwd"])
-    t_step = 0.0
-    t_phase = [0.0] * len(names)
     with sampler:
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        for _ in range(args.steps):
-            if not args.no_flush:
-                flush.zero_()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e3 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            _, evs = step(coords, up, feats if gravnet else None, up_agg if gravnet else None)
-            e3.record(stream)
-            e3.synchronize()
-            t_step += e0.elapsed_time(e3)
-            marks = [e0] + evs + [e3]
-            for i in range(len(names)):
-                t_phase[i] += marks[i].elapsed_time(marks[i + 1])
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
+        t_step, t_phase = timed_steps(step, args.steps, 0, stream, flush, world)
     launches = _lib.launch_count() - launches0
     clocks = sampler.summary()
 
@@ -392,9 +516,9 @@ def main():
             if gravnet:
                 gf, gd = ops.gravnet_aggregate_grad(d_late[0], d_first[1], idx, d2, 10.0, [0, 1],
                                                     True, so)
-                bwd_outs = [ops.binned_select_knn_grad(gd, idx, c, so), gf]
+                bwd_outs = [ops.binned_select_knn_grad(gd, idx, c, so, det), gf]
             else:
-                bwd_outs = [ops.binned_select_knn_grad(d_late[0], idx, c, so)]
+                bwd_outs = [ops.binned_select_knn_grad(d_late[0], idx, c, so, det)]
             ev_bwd = torch.cuda.Event()
             ev_bwd.record(stream)
             outs = fwd_outs + bwd_outs
@@ -416,11 +540,9 @@ def main():
         torch.cuda.synchronize()
         h_out = [torch.empty(o.shape, dtype=o.dtype).pin_memory() for o in outs]
         e2e_steps = max(1, min(args.steps, 10))
-        # latency: each step on its own (its outputs back on the host before the
-        # next one starts)
         t_lat = 0.0
-        for it in range(e2e_steps + 1):
-            if not args.no_flush:
+        for it in range(e2e_steps + 1):  # one step alone: outputs on the host before the next
+            if flush is not None:
                 flush.zero_()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
@@ -431,17 +553,15 @@ def main():
             if it > 0:  # first iteration warms the pinned paths
                 t_lat += e0.elapsed_time(e1)
         lat_ms = t_lat / e2e_steps
-        # throughput: the steps back to back, as a training loop runs them -- step
-        # i's outputs stream back while step i+1's inputs arrive and it computes
-        # (every step still copies all its inputs in and all its outputs out)
-        # (at most two steps in flight: step i waits for step i-2's copies, so
-        # the caching allocator recycles output blocks instead of growing)
+
+        # steps back to back, at most two in flight (step i waits for step i-2's
+        # copies, so the caching allocator recycles output blocks)
         def pipelined(n_steps):
             done = []
             for it in range(n_steps):
                 if it >= 2:
                     stream.wait_event(done[it - 2])
-                if not args.no_flush:
+                if flush is not None:
                     flush.zero_()
                 e2e_step(h_out, join=False)
                 ev = torch.cuda.Event()
@@ -449,8 +569,10 @@ def main():
                 done.append(ev)
             stream.wait_stream(s_d2h)
 
-        pipelined(3)  # warm-up: the allocator's blocks for two steps in flight
+        pipelined(3)
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -462,9 +584,9 @@ def main():
         d2h = sum(h.numel() * h.element_size() for h in h_out)
         e2e = [e2e_ms, h2d, d2h, lat_ms]
 
-    per_rank = [t_step / args.steps, n, e2e[0] if e2e else 0.0, e2e[3] if e2e else 0.0] + \
-        [t / args.steps for t in t_phase]
+    per_rank = [t_step, n, e2e[0] if e2e else 0.0, e2e[3] if e2e else 0.0] + list(t_phase)
     allr = sharding.gather_floats(per_rank)
+    strong = None if args.no_strong else strong_scaling(args, rank, world, dev, flush)
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -484,37 +606,49 @@ def main():
         b_bwd += (8 * n * k + 4 * n * k * F + 8 * n * F) + (8 * n * F + 8 * n * k + 8 * n * k * F + 4 * n * k)
     t_knn_ms = phase["knn_gravnet_fwd" if gravnet else "knn_fwd"]
     b_phase = b_fwd
-    if gravnet:  # the fused op also does the aggregation forward: 8Nk + 4NkF + 8NF
+    compulsory = 4 * n * d + 8 * n * k  # coords in, idx + d2 out
+    if gravnet:  # the op also does the aggregation forward: 8Nk + 4NkF + 8NF
         b_phase += 8 * n * k + 4 * n * k * 64 + 8 * n * 64
+        compulsory += 4 * n * 64 + 4 * n * 128
     achieved = b_phase / (t_knn_ms * 1e-3) / 1e9
+    traffic = load_traffic(args.config)
+    roof = {"bound": "hbm",
+            "kernel": ("knn_gravnet (k_tiles + k_tile_search + k_tile_finish + redo, then the "
+                       "aggregation)") if gravnet else
+                      "binned_select_knn (k_tiles + k_tile_search + k_tile_finish + k_knn_fwd redo)",
+            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "frac_kind": "model: SURVEY 8(d) algorithmic bytes (counts the reference algorithm's "
+                         "candidate reads, which these kernels serve from L2/shared memory) / "
+                         "measured time; not a DRAM measurement",
+            "bytes_model": "B_fwd = 4Nd + 4d*C_total + 8Nk "
+                           f"(C_total={c_total:.3g}) per launch"
+                           + (" + GravNet fwd 8Nk + 4NkF + 8NF" if gravnet else ""),
+            "compulsory_bytes": compulsory,
+            "compulsory_frac": compulsory / (t_knn_ms * 1e-3) / 1e9 / peak,
+            "traffic": traffic,
+            "dram_frac": (traffic / (t_knn_ms * 1e-3) / 1e9 / peak) if traffic else None,
+            "traffic_source": "ncu dram__bytes_read+write of the search kernels "
+                              "(profiles/ncu_summary.json, same build)",
+            "binding": "SM instruction issue / latency (ncu: k_tile_search and k_tile_finish "
+                       "SM throughput ~70%, DRAM < 15%; profiles/)",
+            "peak_source": peak_src,
+            "step_frac_model": (b_fwd + b_bwd) / (ms * 1e-3) / 1e9 / peak}
     line = {
         "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (reference generate_dataset, seed per rank, cast to float32)",
-        "config": {"workload": desc, "n_points_per_gpu": n, "d": d, "k": k, "n_bins": n_bins,
-                   "d_bin": d_bin, "events": world if scaling == "weak" else 64,
-                   "l2": "no flush" if args.no_flush else "flushed (256 MiB write) before every step",
-                   "precision": "fp32 distance filter, float64 exact epilogue / gradient sums"},
+        "config": {**config_keys(args.config, n, d, k, n_bins,
+                                 world if scaling == "weak" else 64, not args.no_flush),
+                   "precision": "fp32 distance filter, float64 exact epilogue / gradient terms",
+                   "backward": "deterministic transposed" if det else "compensated fp32x4 atomics"},
         "breakdown_ms": phase,
-        "roofline": {"bound": "hbm",
-                     "kernel": ("knn_gravnet (k_tiles + k_tile_search + k_tile_finish + redo, then"
-                                " the aggregation)") if gravnet else
-                               "binned_select_knn (k_tiles + k_tile_search + k_tile_finish + "
-                               "k_knn_fwd redo)",
-                     "note": "achieved = the reference algorithm's bytes (SURVEY 8(d)) / time; "
-                             "frac > 1 means the kernels serve those candidate reads from "
-                             "L2/shared memory: traffic is what they take from DRAM",
-                     "achieved": achieved, "peak": peak,
-                     "unit": "GB/s", "frac": achieved / peak, "traffic": load_traffic(args.config),
-                     "peak_source": peak_src,
-                     "bytes_model": "SURVEY 8(d) B_fwd = 4Nd + 4d*C_total + 8Nk "
-                                    f"(C_total={c_total:.3g}) per launch"
-                                    + (" + GravNet fwd 8Nk + 4NkF + 8NF (fused)" if gravnet else ""),
-                     "step_frac": (b_fwd + b_bwd) / (ms * 1e-3) / 1e9 / peak},
+        "roofline": roof,
         "gpu_launches": int(launches),
         "clocks": clocks,
     }
+    if strong:
+        line["strong_scaling"] = strong
     if e2e:
         e2e_ms = float(allr[:, 2].max())
         line["e2e"] = {"value": total_q / (e2e_ms * 1e-3), "unit": "queries/s",
@@ -525,10 +659,10 @@ def main():
                        "latency_ms_per_step": float(allr[:, 3].max())}
     if world == 1 and not args.no_cpu_baseline:
         try:
-            tt, det = cpu_reference_step(coords_np, off_np, k, n_bins,
-                                         query_frac=REF_QUERY_FRAC.get(args.config, 1.0))
-            line["cpu_baseline"] = {"value": n / tt, "unit": "queries/s", "cores": det["cores"],
-                                    "kind": det["kind"], "sample": det["sample"]}
+            tt, rate, det_ = cpu_reference_step(coords_np, off_np, k, n_bins,
+                                                REF_QUERY_FRAC.get(args.config, 1.0))
+            line["cpu_baseline"] = {"value": rate, "unit": "queries/s", "cores": det_["cores"],
+                                    "kind": det_["kind"], "sample": det_["sample"]}
         except Exception as exc:  # the baseline must not kill the GPU number
             line["cpu_baseline"] = {"value": None, "unit": "queries/s", "cores": os.cpu_count(),
                                     "kind": "unavailable", "sample": repr(exc)}
