@@ -62,7 +62,6 @@ enum fg_status {
                                     otherwise float (= float32 of the reference d2)         */
 #define FG_KNN_STATS 0x100       /* diagnostics: count search events (fg_knn_stats)        */
 #define FG_KNN_NO_TILE 0x200     /* diagnostics: skip the lane-per-query tile path         */
-#define FG_KNN_FUSED_GN 0x400    /* fg_knn_gravnet_fwd_ws: aggregate inside the tile epilogue */
 #define FG_KNN_FUSED_EPI 0x800   /* diagnostics: tile epilogue inside the scan kernel      */
 
 /* Reducer codes for the GravNet aggregation (G/gravnet.py:26, order = blocks). */
@@ -180,14 +179,10 @@ int fg_gravnet_bwd_workspace_size(int64_t n, int32_t n_feats, int32_t k, size_t 
 
 /* Fused search + GravNet aggregation (the fusion the paper
  * describes): binned_select_knn (float32 distances, no mask /
- * radius) and gravnet_aggregate of its rows in one pass -- the tile path
- * aggregates every row it writes straight from its staged row, the rows it
- * leaves to the warp-per-query kernel are aggregated afterwards.  Outputs are
- * those of fg_knn_fwd_ws + fg_gravnet_fwd (scratch: fg_knn_workspace_size with
- * the same flags).  The in-epilogue fusion runs with FG_KNN_FUSED_GN (tile path,
- * F even and <= 64); by default the op runs exactly that pair, which is faster
- * on B200 (the aggregation needs more gathers in flight than the
- * tile kernel's occupancy allows). */
+ * radius) then gravnet_aggregate of its rows in sorted order, one call on one
+ * stream.  Outputs are those of fg_knn_fwd_ws + fg_gravnet_fwd (scratch:
+ * fg_knn_workspace_size with the same flags).  (An in-epilogue fusion was
+ * slower on B200 and removed: DESIGN.md 5.) */
 int fg_knn_gravnet_fwd_ws(const float *sorted_coords, const int32_t *sort_order,
                           const int64_t *bin_idx, const int32_t *bin_bounds,
                           const int64_t *row_splits, const double *dim_mins, const double *widths,

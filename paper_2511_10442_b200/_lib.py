@@ -23,7 +23,6 @@ FG_KNN_EXHAUSTIVE = 0x4
 FG_KNN_D2_F64 = 0x8
 FG_KNN_STATS = 0x100
 FG_KNN_NO_TILE = 0x200
-FG_KNN_FUSED_GN = 0x400
 FG_KNN_FUSED_EPI = 0x800
 FG_BWD_F64 = 0x1
 FG_BWD_DETERMINISTIC = 0x2

@@ -52,19 +52,10 @@ struct GnArgs {
     int n_red;
     int include_self;
     const int32_t* order;
-    // optional device row list: rows psid[plist[i]], i < *pcount (the tile
-    // search's redo list, in sorted positions)
-    const int32_t* plist = nullptr;
-    const int* pcount = nullptr;
-    const int32_t* psid = nullptr;
 };
 
 __device__ __forceinline__ int64_t row_of(const GnArgs& g, int64_t p) {
     return g.order ? (int64_t)g.order[p] : p;
-}
-__device__ __forceinline__ int64_t row_of_list(const GnArgs& g, int64_t p) {
-    if (g.plist) return (int64_t)g.psid[g.plist[p]];
-    return row_of(g, p);
 }
 
 __device__ __forceinline__ bool is_max(const GnArgs& g, int b) { return (g.max_bits >> b) & 1u; }
@@ -137,7 +128,7 @@ __device__ __forceinline__ void gather(const GnArgs& g, const Window& wd, int j0
 template <int VW, int UF>
 __device__ __forceinline__ void gn_fwd_row(const GnArgs& g, int f0, float* __restrict__ out, int64_t p) {
     const int lane = lane_id();
-    const int64_t v = row_of_list(g, p);
+    const int64_t v = row_of(g, p);
     const int k = g.k, F = g.F, W = F * g.n_red;
     const int fl = f0 + lane * VW;
     const bool lane_on = fl < F;
@@ -182,7 +173,7 @@ template <int VW>
 __global__ void __launch_bounds__(kRowWarps * 32) k_gn_fwd(const GnArgs g, int f0, float* __restrict__ out) {
     constexpr int UF = FG_GN_FWD_U;  // gathers in flight per warp
     const int lane = lane_id();
-    const int64_t n_rows = g.pcount ? (int64_t)*g.pcount : g.n;
+    const int64_t n_rows = g.n;
     for (int64_t p = blockIdx.x * (int64_t)kRowWarps + (threadIdx.x >> 5); p < n_rows;
          p += (int64_t)gridDim.x * kRowWarps)
         gn_fwd_row<VW, UF>(g, f0, out, p);
@@ -745,28 +736,6 @@ int gn_backward(const GnArgs& g, GnBwd bw, const BwdWs& w, cudaStream_t st) {
         FG_TRY(launched(st));
     }
     return 0;
-}
-
-// Aggregation of the rows psid[plist[i]], i < *pcount (device count): the
-// rows the fused tile search left to the warp-per-query kernel.
-int launch_fwd_list(const float* feats, int64_t n, int F, const int32_t* idx, const float* d2, int k,
-                    double scale, const int32_t* reducers, int n_red, int include_self,
-                    const int32_t* plist, const int* pcount, const int32_t* psid, float* out,
-                    cudaStream_t st) {
-    GnArgs g;
-    FG_TRY(check_reducers(reducers, n_red, g));
-    g.feats = feats; g.n = n; g.F = F; g.idx = idx; g.d2 = d2; g.k = k;
-    g.scale = scale; g.include_self = include_self; g.order = nullptr;
-    g.plist = plist; g.pcount = pcount; g.psid = psid;
-    const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(n, kRowWarps), 148 * 8);
-    return with_vw(pick_vw(F, {feats, out}), [&](auto vw) {
-        constexpr int VW = decltype(vw)::value;
-        for (int f0 = 0; f0 < F; f0 += 32 * VW) {
-            k_gn_fwd<VW><<<blocks, kRowWarps * 32, 0, st>>>(g, f0, out);
-            FG_TRY(launched(st));
-        }
-        return 0;
-    });
 }
 
 int reducer_bits(const int32_t* reducers, int n_red, unsigned* bits) {

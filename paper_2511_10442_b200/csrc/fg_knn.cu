@@ -11,10 +11,6 @@ namespace tile {
 int launch(TileArgs& t, const search::KnnArgs& a, int d_bin, cudaStream_t st);
 }
 namespace gravnet {
-int launch_fwd_list(const float* feats, int64_t n, int F, const int32_t* idx, const float* d2, int k,
-                    double scale, const int32_t* reducers, int n_red, int include_self,
-                    const int32_t* plist, const int* pcount, const int32_t* psid, float* out,
-                    cudaStream_t st);
 int reducer_bits(const int32_t* reducers, int n_red, unsigned* bits);
 }  // namespace gravnet
 }  // namespace fg
@@ -60,18 +56,6 @@ int check_args(const float* sorted_coords, const int32_t* sort_order, const int6
     if ((flags & FG_KNN_USE_DIRECTION) && !dir_mask) return FG_ERR_NULL;
     return 0;
 }
-
-// Fused GravNet request for the current call (set by fg_knn_gravnet_fwd_ws
-// around its call of fg_knn_fwd_ws; thread-local, so concurrent host threads
-// do not interfere).
-struct FusedGn {
-    const float* feats;
-    float* out;
-    int F, n_red, include_self;
-    unsigned max_bits;
-    double scale;
-};
-thread_local const FusedGn* g_fused = nullptr;
 
 struct TileWs {
     int* ctr;
@@ -192,15 +176,6 @@ extern "C" int fg_knn_fwd_ws(const float* sorted_coords, const int32_t* sort_ord
         if (!workspace) return FG_ERR_NULL;
         if (workspace_bytes < w.bytes) return FG_ERR_WORKSPACE;
         tile::TileArgs t{};
-        if (g_fused) {  // fg_knn_gravnet_fwd_ws: aggregate every row the tiles write
-            t.gn_feats = g_fused->feats;
-            t.gn_out = g_fused->out;
-            t.gn_F = g_fused->F;
-            t.gn_n_red = g_fused->n_red;
-            t.gn_incl = g_fused->include_self;
-            t.gn_max_bits = g_fused->max_bits;
-            t.gn_scale = g_fused->scale;
-        }
         t.sc = a.sc;
         t.sid = sort_order;
         t.bounds = bin_bounds;
@@ -218,7 +193,7 @@ extern "C" int fg_knn_fwd_ws(const float* sorted_coords, const int32_t* sort_ord
         t.redo = w.redo;
         t.out_idx = out_idx;
         t.out_d2 = reinterpret_cast<float*>(out_d2);
-        const bool split = !(flags & FG_KNN_FUSED_EPI) && !g_fused;
+        const bool split = !(flags & FG_KNN_FUSED_EPI);
         t.lists = split ? w.lists : nullptr;
         t.meta = split ? w.meta : nullptr;
         t.stats = a.stats ? a.stats + ST_COUNT : nullptr;
@@ -264,34 +239,15 @@ extern "C" int fg_knn_gravnet_fwd_ws(const float* sorted_coords, const int32_t* 
                       out_d2));
     if (n == 0) return 0;
     if (!feats || !agg_out) return FG_ERR_NULL;
-    cudaStream_t st = (cudaStream_t)stream;
-    // In-epilogue fusion is opt-in (FG_KNN_FUSED_GN): measured on B200 (config E)
-    // the tile kernel's 16 warps/SM cannot keep enough feature gathers in flight,
-    // fused 3.2 ms vs 1.27 + 0.94 ms for the two kernels -- so by default the op
-    // runs the search and then the high-occupancy aggregation kernel.
-    const bool fuse = (flags & FG_KNN_FUSED_GN) &&
-                      tile_path(n_coords, n_splits, d_bin, n_bins, k, flags & ~FG_KNN_FUSED_GN) &&
-                      n_feats % 2 == 0 && n_feats <= 64 && ((uintptr_t)feats % 8) == 0 &&
-                      ((uintptr_t)agg_out % 8) == 0;
-    flags &= ~FG_KNN_FUSED_GN;
-    if (!fuse) {  // the search, then the aggregation (same results)
-        FG_TRY(fg_knn_fwd_ws(sorted_coords, sort_order, bin_idx, bin_bounds, row_splits, dim_mins,
-                             widths, n, n_coords, n_splits, d_bin, n_bins, k, nullptr, 0.0, flags,
-                             out_idx, out_d2, workspace, workspace_bytes, stream));
-        return fg_gravnet_fwd(feats, n, n_feats, out_idx, out_d2, k, weight_scale, reducers,
-                              n_reducers, include_self, sort_order, agg_out, stream);
-    }
-    FusedGn fg_req{feats, agg_out, n_feats, n_reducers, include_self, bits, weight_scale};
-    g_fused = &fg_req;
-    const int rc = fg_knn_fwd_ws(sorted_coords, sort_order, bin_idx, bin_bounds, row_splits,
-                                 dim_mins, widths, n, n_coords, n_splits, d_bin, n_bins, k,
-                                 nullptr, 0.0, flags, out_idx, out_d2, workspace, workspace_bytes,
-                                 stream);
-    g_fused = nullptr;
-    FG_TRY(rc);
-    // rows the tiles left to the warp-per-query kernel: aggregate them now
-    const TileWs w = tile_ws(workspace, n, n_splits, d_bin, n_bins);
-    return fg::gravnet::launch_fwd_list(feats, n, n_feats, out_idx, out_d2, k, weight_scale,
-                                        reducers, n_reducers, include_self, w.redo, &w.ctr[2],
-                                        sort_order, agg_out, st);
+    // the search, then the high-occupancy aggregation kernel over its rows in
+    // sorted order.  An in-epilogue fusion (aggregating each row inside the
+    // tile search's epilogue, skipping the (N, k) round trip) was measured on
+    // B200 at 3.12 ms vs 1.27 + 0.94 ms for this pair on config E -- the
+    // aggregation is a 5 GB feature gather that needs the memory-level
+    // parallelism of its own kernel -- and was removed.
+    FG_TRY(fg_knn_fwd_ws(sorted_coords, sort_order, bin_idx, bin_bounds, row_splits, dim_mins, widths,
+                         n, n_coords, n_splits, d_bin, n_bins, k, nullptr, 0.0, flags, out_idx, out_d2,
+                         workspace, workspace_bytes, stream));
+    return fg_gravnet_fwd(feats, n, n_feats, out_idx, out_d2, k, weight_scale, reducers, n_reducers,
+                          include_self, sort_order, agg_out, stream);
 }

@@ -93,12 +93,6 @@ struct TileArgs {
     // list (sorted positions, kCap per query) and (tau, m); k_tile_finish sorts
     int32_t* lists;
     float2* meta;
-    // fused GravNet aggregation of every row the tile path writes (null: off)
-    const float* gn_feats;  // (n, gn_F) in original order
-    float* gn_out;          // (n, gn_F * gn_n_red)
-    int gn_F, gn_n_red, gn_incl;
-    unsigned gn_max_bits;
-    double gn_scale;
 };
 
 // Per-warp shared memory of the scan.
@@ -111,7 +105,7 @@ struct ScanWarp {
     alignas(16) uint16_t scode[64];       // ring codes
 };
 // ... plus the epilogue staging when the scan kernel finishes its own queries
-// (FG_KNN_FUSED_EPI, fused GravNet).
+// (FG_KNN_FUSED_EPI, a diagnostics variant).
 struct TileWarp : ScanWarp {
     float skey[kCap];                     // epilogue staging of one query: keys
     int32_t sid[kCap];                    //   and original ids, in bucket order
@@ -597,61 +591,6 @@ __device__ __forceinline__ void push_redo(const TileArgs& a, bool redo, int32_t 
 // __match_any groups; odd-even transposition inside buckets; equal float32
 // keys among the decided entries -> exact path; the sorted row (self first) is
 // written coalesced.  Returns false when the query must be redone.
-// GravNet aggregation (G/gravnet.py:64-97) of row `qid` straight from the
-// staged row (slot 0 = self, d2 as the float32 written to out_d2): weights
-// exp(-scale d2) and all sums / maxima in float64, slots in order, lanes over
-// features (2 per lane, F <= 64), 4 gathers in flight -- the same arithmetic and
-// order as fg_gravnet_fwd, without re-reading the (N, k) neighbour matrix.
-template <class WS>
-__device__ __forceinline__ void fused_gravnet(const TileArgs& a, const WS& W, int32_t qid) {
-    const int lane = lane_id();
-    const int k = a.k, F = a.gn_F;
-    const int s_begin = a.gn_incl ? 0 : 1;
-    const int cnt = k - s_begin;
-    const int fl = 2 * lane;
-    const bool lane_on = fl < F;
-    double sum[2] = {0.0, 0.0}, mx[2] = {-INFINITY, -INFINITY};
-    for (int base = 0; base < k; base += 32) {
-        const int s = base + lane;
-        const bool ok = s >= s_begin && s < k;
-        const double wl = ok ? exp(-a.gn_scale * (double)W.okey[s]) : 0.0;
-        const int32_t ul = ok ? W.oid[s] : 0;
-        const int nwin = min(32, k - base);
-        for (int j0 = 0; j0 < nwin; j0 += 4) {
-            float2 x[4];
-            double w[4];
-            bool valid[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int jj = j0 + q;
-                valid[q] = jj < nwin && base + jj >= s_begin;
-                const int32_t u = __shfl_sync(FG_FULL_MASK, ul, jj & 31);
-                w[q] = __shfl_sync(FG_FULL_MASK, wl, jj & 31);
-                x[q] = make_float2(0.f, 0.f);
-                if (valid[q] && lane_on)
-                    x[q] = __ldg(reinterpret_cast<const float2*>(a.gn_feats + (int64_t)u * F + fl));
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                if (!valid[q]) continue;
-                const double t0 = w[q] * (double)x[q].x, t1 = w[q] * (double)x[q].y;
-                sum[0] += t0;
-                sum[1] += t1;
-                mx[0] = t0 > mx[0] ? t0 : mx[0];
-                mx[1] = t1 > mx[1] ? t1 : mx[1];
-            }
-        }
-    }
-    if (!lane_on) return;
-    const int Wd = F * a.gn_n_red;
-    for (int b = 0; b < a.gn_n_red; ++b) {
-        const bool is_max = (a.gn_max_bits >> b) & 1u;
-        const float o0 = cnt > 0 ? (float)(is_max ? mx[0] : sum[0] / (double)cnt) : 0.0f;
-        const float o1 = cnt > 0 ? (float)(is_max ? mx[1] : sum[1] / (double)cnt) : 0.0f;
-        *reinterpret_cast<float2*>(a.gn_out + (int64_t)qid * Wd + (int64_t)b * F + fl) = make_float2(o0, o1);
-    }
-}
-
 constexpr int kRounds = (kCap + 31) / 32;
 #ifndef FG_FINISH_MATCH
 #define FG_FINISH_MATCH 0
@@ -833,7 +772,6 @@ __device__ __forceinline__ bool finish_query(WS& W, const TileArgs& a, int j, co
             od[sl] = W.okey[sl];
         }
     }
-    if (a.gn_feats) fused_gravnet(a, W, qid);
     __syncwarp();
     return true;
 }

@@ -17,9 +17,9 @@ import torch
 from torch import nn
 
 from . import ops
-from .core import NeighborMatrix
+from .binning import BinningConfig, build_bin_index
+from .core import NeighborMatrix, PointCloud
 from .errors import BadShapeError, ShapeMismatchError
-from .knn import select_knn
 
 _REDUCERS = ("mean", "max")
 _CODES = {"mean": 0, "max": 1}
@@ -117,8 +117,20 @@ class GravNetOp(nn.Module):
             self.out = nn.Linear(in_features + n_prop * len(reducers), out_features)
 
     def aggregate(self, coords: torch.Tensor, feats: torch.Tensor, row_splits):
-        idx, d2, order = select_knn(coords, row_splits, self.k, return_order=True)
-        agg = gravnet_aggregate(feats, NeighborMatrix(idx, d2), self.spec, order)
+        """Bin the learned coordinates, then ONE call of the fused op
+        ``fastgraph::knn_gravnet`` (search + aggregation of its rows in sorted
+        order; autograd into coords through d2 and into feats)."""
+        cloud = PointCloud(coords, row_splits, check_finite=False)
+        index = build_bin_index(cloud, BinningConfig(k_target=self.k))
+        if feats.shape[0] != cloud.n_vertices:
+            raise ShapeMismatchError(f"features cover {feats.shape[0]} vertices, "
+                                     f"coords have {cloud.n_vertices}")
+        rs = cloud.row_splits.device_tensor(cloud.coords.device)
+        idx, d2, agg = ops.knn_gravnet(cloud.coords, rs, index.bin_idx, index.sort_order,
+                                       index.bin_bounds, index.dim_mins, index.widths,
+                                       index.sorted_coords, self.k, index.d_bin, index.n_bins,
+                                       feats, float(self.spec.weight_scale), self.spec.codes,
+                                       bool(self.spec.include_self))
         return agg, idx, d2
 
     def forward(self, x: torch.Tensor, row_splits, feats: torch.Tensor | None = None):

@@ -330,13 +330,10 @@ gravnet_aggregate.register_autograd(_gn_backward, setup_context=_gn_setup)
 def knn_gravnet(coords: Tensor, row_splits: Tensor, bin_idx: Tensor, sort_order: Tensor,
                 bin_bounds: Tensor, dim_mins: Tensor, widths: Tensor, sorted_coords: Tensor,
                 K: int, d_bin: int, n_bins: int, feats: Tensor, weight_scale: float,
-                reducers: list[int], include_self: bool,
-                fuse_epilogue: bool = False) -> tuple[Tensor, Tensor, Tensor]:
+                reducers: list[int], include_self: bool) -> tuple[Tensor, Tensor, Tensor]:
     """binned_select_knn (float32 distances) + gravnet_aggregate of its rows
-    (SURVEY 8(f) item 1): -> (idx, d2, aggregated features), differentiable
-    w.r.t. coords and feats.  ``fuse_epilogue`` aggregates inside the tile
-    search's epilogue (the paper's fusion); the default runs the two kernels,
-    which is faster on B200.  Same values either way."""
+    (the GravNetOp forward): -> (idx, d2, aggregated
+    features) from one C-ABI call, differentiable w.r.t. coords and feats."""
     _require_cuda(coords, sorted_coords, feats)
     L = _lib.load()
     dev = sorted_coords.device
@@ -348,7 +345,7 @@ def knn_gravnet(coords: Tensor, row_splits: Tensor, bin_idx: Tensor, sort_order:
     F = feats.shape[1]
     f = feats.to(torch.float32).contiguous()
     red = _check_red(reducers)
-    flags = _DEBUG_FLAGS | (_lib.FG_KNN_FUSED_GN if fuse_epilogue else 0)
+    flags = _DEBUG_FLAGS
     idx = torch.empty((n, K), dtype=torch.int32, device=dev)
     d2 = torch.empty((n, K), dtype=torch.float32, device=dev)
     agg = torch.empty((n, F * red.numel()), dtype=torch.float32, device=dev)
@@ -364,7 +361,7 @@ def knn_gravnet(coords: Tensor, row_splits: Tensor, bin_idx: Tensor, sort_order:
 
 @knn_gravnet.register_fake
 def _kg_fake(coords, row_splits, bin_idx, sort_order, bin_bounds, dim_mins, widths, sorted_coords,
-             K, d_bin, n_bins, feats, weight_scale, reducers, include_self, fuse_epilogue=False):
+             K, d_bin, n_bins, feats, weight_scale, reducers, include_self):
     n = coords.shape[0]
     return (coords.new_empty((n, K), dtype=torch.int32),
             coords.new_empty((n, K), dtype=torch.float32),
@@ -388,7 +385,7 @@ def _kg_backward(ctx, grad_idx, grad_d2, grad_agg):
         gd = gd_agg if gd is None else gd + gd_agg
         gf = gf.to(ctx.dtypes[1])
     gc = None if gd is None else binned_select_knn_grad(gd, idx, coords, order).to(ctx.dtypes[0])
-    return (gc,) + (None,) * 10 + (gf, None, None, None, None)
+    return (gc,) + (None,) * 10 + (gf, None, None, None)
 
 
 knn_gravnet.register_autograd(_kg_backward, setup_context=_kg_setup)

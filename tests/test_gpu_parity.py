@@ -386,6 +386,33 @@ def test_gravnet_autograd_and_op():
     assert layer.space.weight.grad is not None and layer.space.weight.grad.abs().sum() > 0
 
 
+def test_gravnet_layer_vs_oracle_chain(oracle):
+    """GravNetOp (raw op, linear=False) forward and backward against the oracle
+    chain: canonical kNN -> gravnet_aggregate -> its backward -> knn_backward
+    (G/gravnet.py:75-150, G/knn.py:135-168), two row splits."""
+    rng = np.random.default_rng(21)
+    n, k, F = 6000, 12, 16
+    coords = rng.random((n, 4)).astype(np.float32)
+    off = np.array([0, 2500, n], np.int64)
+    feats = rng.standard_normal((n, F)).astype(np.float32)
+    up = rng.standard_normal((n, 2 * F)).astype(np.float32)
+    layer = fg.GravNetOp(k=k, linear=False)
+    c = torch.from_numpy(coords).to(dev()).requires_grad_(True)
+    f = torch.from_numpy(feats).to(dev()).requires_grad_(True)
+    agg, idx, d2 = layer.aggregate(c, f, off)
+    (agg * torch.from_numpy(up).to(dev())).sum().backward()
+    oi, od = oracle.knn_canonical(coords.astype(np.float64), off, k)
+    assert np.array_equal(idx.cpu().numpy(), oi)
+    od32 = od.astype(np.float32)
+    assert np.array_equal(d2.detach().cpu().numpy(), od32)
+    oa = oracle.gravnet_aggregate(feats, oi, od32, 10.0)
+    np.testing.assert_allclose(agg.detach().cpu().numpy(), oa, rtol=1e-5, atol=1e-6)
+    ogf, ogd = oracle.gravnet_aggregate_backward(feats, oi, od32, up, 10.0, ("mean", "max"), True)
+    np.testing.assert_allclose(f.grad.cpu().numpy(), ogf, rtol=1e-5, atol=1e-6)
+    ogc = oracle.knn_backward(coords.astype(np.float64), oi, ogd.astype(np.float32).astype(np.float64))
+    np.testing.assert_allclose(c.grad.cpu().numpy(), ogc, rtol=1e-4, atol=1e-5 * np.abs(ogc).max())
+
+
 def test_cpu_tensor_raises():
     with pytest.raises(fg.errors.BackendUnavailableError):
         ops.bin_by_coordinates(torch.zeros(4, 2), torch.tensor([0, 4]), 2, 5)

@@ -91,7 +91,7 @@ def test_tile_equals_warp_kernel_full_size(cfg):
 
 
 # ---------------------------------------------------------------- fused search + GravNet
-def _fused_and_pair(c32, off, k, F, reducers, incl, seed=0, fuse=True):
+def _fused_and_pair(c32, off, k, F, reducers, incl, seed=0):
     n, d = c32.shape
     nb = fg.compute_n_bins(int(np.diff(off).max()), k, d)
     ct = torch.from_numpy(np.ascontiguousarray(c32)).cuda()
@@ -100,7 +100,7 @@ def _fused_and_pair(c32, off, k, F, reducers, incl, seed=0, fuse=True):
     feats = torch.from_numpy(np.random.default_rng(seed).standard_normal((n, F))
                              .astype(np.float32)).cuda()
     i1, d1, a1 = ops.knn_gravnet(ct, rs, bi, so, bb, mi, wi, sc, k, d, nb, feats, 10.0, reducers,
-                                 incl, fuse)
+                                 incl)
     i0, d0 = ops.binned_select_knn(ct, rs, bi, so, bb, mi, wi, sc, k, d, nb, None, None, False,
                                    False)
     a0 = ops.gravnet_aggregate(feats, i0, d0, 10.0, reducers, incl, so)
@@ -108,13 +108,15 @@ def _fused_and_pair(c32, off, k, F, reducers, incl, seed=0, fuse=True):
     return (i0, d0, a0), (i1, d1, a1), feats
 
 
-@pytest.mark.parametrize("F,reducers,incl,fuse", [(64, [0, 1], True, True), (32, [1], False, True),
-                                                 (8, [0], True, True), (65, [0, 1], True, True),
-                                                 (64, [0, 1], True, False)])
-def test_fused_knn_gravnet_equals_ops(oracle, F, reducers, incl, fuse):
-    c, off = generate_dataset(20_000, 4, 2, 11, "uniform")
+@pytest.mark.parametrize("F,reducers,incl,dist", [(64, [0, 1], True, "uniform"),
+                                                 (32, [1], False, "uniform"),
+                                                 (8, [0], True, "uniform"), (65, [0, 1], True, "uniform"),
+                                                 (64, [0, 1], True, "clusters")])
+def test_fused_knn_gravnet_equals_ops(oracle, F, reducers, incl, dist):
+    """Includes clustered data, where the tile path steps aside."""
+    c, off = generate_dataset(20_000, 4, 2, 11, dist)
     (i0, d0, a0), (i1, d1, a1), feats = _fused_and_pair(c.astype(np.float32), off, 40, F, reducers,
-                                                        incl, fuse=fuse)
+                                                        incl)
     assert torch.equal(i0, i1) and torch.equal(d0, d1)
     np.testing.assert_allclose(a1.cpu().numpy(), a0.cpu().numpy(), rtol=1e-6, atol=1e-7)
     names = ["mean" if r == 0 else "max" for r in reducers]
@@ -136,8 +138,7 @@ def test_fused_knn_gravnet_full_size_and_grad():
     f = feats[:50_000].clone().requires_grad_(True)
     bi, so, bb, mi, wi, sc = ops.bin_by_coordinates(ct.detach(), rs, d, nb)
     up = torch.randn(50_000, 128, device="cuda")
-    _, d2f, af = ops.knn_gravnet(ct, rs, bi, so, bb, mi, wi, sc, k, d, nb, f, 10.0, [0, 1], True,
-                                 True)
+    _, d2f, af = ops.knn_gravnet(ct, rs, bi, so, bb, mi, wi, sc, k, d, nb, f, 10.0, [0, 1], True)
     (af * up).sum().backward()
     gc1, gf1 = ct.grad.clone(), f.grad.clone()
     ct.grad = None
