@@ -14,18 +14,15 @@ int launch_db(TileArgs& t, const search::KnnArgs& a, cudaStream_t st) {
     FG_CUDA(cudaMemsetAsync(t.ctr, 0, 8 * sizeof(int), st));
     k_tiles<DB><<<(unsigned)ceil_div(t.n_blocks, 4), 128, 0, st>>>(t);
     FG_TRY(launched(st));
-    static int sms = 0;  // per template instance: also sets the smem opt-ins once
-    if (!sms) {
-        int dev = 0;
-        FG_CUDA(cudaGetDevice(&dev));
-        FG_CUDA(cudaFuncSetAttribute(k_tile_search<DB, false>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)tile_smem_bytes<false>()));
-        FG_CUDA(cudaFuncSetAttribute(k_tile_search<DB, true>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)tile_smem_bytes<true>()));
-        FG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    }
+    // per call (not cached in a static): the current device's SM count and the
+    // shared-memory opt-ins are per device, and host threads may race on a cache
+    int dev = 0, sms = 0;
+    FG_CUDA(cudaGetDevice(&dev));
+    FG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    FG_CUDA(cudaFuncSetAttribute(k_tile_search<DB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)tile_smem_bytes<false>()));
+    FG_CUDA(cudaFuncSetAttribute(k_tile_search<DB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)tile_smem_bytes<true>()));
     if (t.lists)
         k_tile_search<DB, true><<<(unsigned)(sms * kScanCtasPerSm), kWarps * 32,
                                   tile_smem_bytes<true>(), st>>>(t);

@@ -19,7 +19,7 @@ import torch
 
 from . import ops
 from .core import RowSplits, default_device
-from .errors import BadCapacityError, BadShapeError, ShapeMismatchError
+from .errors import BadCapacityError, BadShapeError, OutOfRangeError, ShapeMismatchError
 
 __all__ = ["Associations", "UniqueObjects", "AssociationMatrices", "find_unique",
            "max_same_count", "oc_helper"]
@@ -137,9 +137,24 @@ def find_unique(assoc: Associations, *, device=None) -> UniqueObjects:
     return _unique_device(assoc, device)
 
 
+def _check_objects(assoc: Associations, unique: UniqueObjects) -> None:
+    """A caller-supplied object list must address existing splits before it
+    reaches the device (the reference raises through RowSplits.bounds,
+    G/core.py:80-84)."""
+    ids, rs = np.asarray(unique.unique_idx), np.asarray(unique.unique_rs_asso)
+    if ids.shape != rs.shape:
+        raise ShapeMismatchError(f"unique_idx has {ids.size} entries, unique_rs_asso {rs.size}")
+    n_splits = assoc.row_splits.n_splits
+    bad = (rs < 0) | (rs >= n_splits)
+    if bad.any():
+        raise OutOfRangeError(f"split {int(rs[bad][0])} out of range [0, {n_splits})")
+
+
 def max_same_count(assoc: Associations, unique: Optional[UniqueObjects] = None, *, device=None):
     """(largest member count, per-object counts in unique order)
     (G/ocgraph.py:137-149)."""
+    if unique is not None:
+        _check_objects(assoc, unique)
     if unique is None or unique.counts is None:
         fresh = _unique_device(assoc, device)
         if unique is None:
@@ -147,9 +162,17 @@ def max_same_count(assoc: Associations, unique: Optional[UniqueObjects] = None, 
         else:  # counts for a caller-supplied object list: same keys, reorder
             pos = {(int(i), int(s)): j for j, (i, s) in
                    enumerate(zip(fresh.unique_idx, fresh.unique_rs_asso))}
-            counts = np.array([fresh.counts[pos[(int(i), int(s))]] if (int(i), int(s)) in pos
-                               else 0 for i, s in zip(unique.unique_idx, unique.unique_rs_asso)],
-                              dtype=np.int64)
+
+            def count(i, s):
+                if (i, s) in pos:
+                    return int(fresh.counts[pos[(i, s)]])
+                # ids the fresh table does not hold (negative / absent): count
+                # them in the split the way the reference does
+                lo, hi = assoc.row_splits.bounds(s)
+                return int(np.count_nonzero(assoc.asso_idx[lo:hi] == i))
+
+            counts = np.array([count(int(i), int(s)) for i, s in
+                               zip(unique.unique_idx, unique.unique_rs_asso)], dtype=np.int64)
             return (int(counts.max()) if counts.size else 0), counts
     counts = np.asarray(unique.counts, dtype=np.int64)
     return (int(counts.max()) if counts.size else 0), counts
@@ -162,6 +185,8 @@ def oc_helper(assoc: Associations, unique: Optional[UniqueObjects] = None, *,
     (G/ocgraph.py:152-202).  Each object scans the first ``n_maxrs`` vertices of
     its split; rows are ascending vertex ids with a contiguous -1 suffix.
     Defaults: n_maxuq = largest member count, n_maxrs = largest split (>= 1)."""
+    if unique is not None:
+        _check_objects(assoc, unique)
     uniq = unique if unique is not None else _unique_device(assoc, device)
     if n_maxuq is None:
         top, _ = max_same_count(assoc, uniq, device=device)

@@ -110,3 +110,20 @@ def test_many_objects_grid_y_loop(oracle):
     ui, ur, _ = oracle.find_unique(asso, off)
     m, mn, v = oracle.oc_helper(asso, off, ui, ur, 2, 64)
     assert np.array_equal(res.m, m) and np.array_equal(res.m_not, mn) and res.visit_count == v
+
+
+def test_caller_objects_validated_and_counted():
+    """a caller-supplied object list is checked on the host (the
+    reference raises OutOfRangeError through RowSplits.bounds, G/core.py:80-84)
+    and counted like the reference's max_same_count (G/ocgraph.py:137-149),
+    including ids the fresh table does not hold (negative background ids)."""
+    asso = np.array([-1, 3, 3, -1, 5, 7, -1, 7], np.int64)
+    a = fg.Associations(asso, fg.RowSplits([0, 4, 8]))
+    bad = fg.UniqueObjects(np.array([3, 7]), np.array([0, 2]))
+    with pytest.raises(fg.errors.OutOfRangeError):
+        fg.oc_helper(a, bad)
+    with pytest.raises(fg.errors.OutOfRangeError):
+        fg.max_same_count(a, fg.UniqueObjects(np.array([3]), np.array([-1])))
+    top, counts = fg.max_same_count(a, fg.UniqueObjects(np.array([3, -1, 7, 9]),
+                                                        np.array([0, 0, 1, 1])))
+    assert counts.tolist() == [2, 2, 2, 0] and top == 2
