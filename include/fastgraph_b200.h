@@ -135,6 +135,19 @@ int fg_knn_fwd_ws(const float *sorted_coords, const int32_t *sort_order, const i
  * Synchronous; not for the hot path. */
 int fg_knn_stats(uint64_t *out, int32_t n, int32_t reset);
 
+/* Brute-force exact kNN (replaces brute_knn / _brute_one, _binned_cy.pyx:335-409;
+ * G/knn.py:118-132) -- the independent GPU verifier: it shares
+ * no code with the binned search.  Every vertex of the query's row split is a
+ * candidate; distances in float64 in the reference's order (pyx:32-48); rows in
+ * the canonical (d2, index) order: slot 0 = self, then the k-1 nearest other
+ * vertices, (-1, 0.0) padding; FG_KNN_USE_DIRECTION / FG_KNN_USE_MAX_R2 as in
+ * fg_knn_fwd.  `queries` (nullable): rows to compute (out rows follow it),
+ * NULL = all n.  k <= 128. */
+int fg_brute_knn(const float *coords, int64_t n, int32_t n_coords, const int64_t *row_splits,
+                 int32_t n_splits, const int32_t *queries, int64_t n_queries,
+                 const int8_t *dir_mask, double max_radius2, uint32_t flags, int32_t k,
+                 int32_t *out_idx, double *out_d2, void *stream);
+
 /* ---------------------------------------------------------------- backward */
 
 int fg_knn_bwd_workspace_size(int64_t n, int32_t n_coords, int32_t k, size_t *bytes);

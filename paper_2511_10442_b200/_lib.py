@@ -36,7 +36,7 @@ EXPORTS = (
     "fg_gravnet_bwd_workspace_size", "fg_gravnet_bwd", "fg_error_string", "fg_abi_version",
     "fg_launch_count", "fg_knn_stats", "fg_knn_workspace_size", "fg_knn_fwd_ws",
     "fg_knn_gravnet_fwd_ws", "fg_oc_unique_workspace_size", "fg_oc_find_unique",
-    "fg_oc_matrices_workspace_size", "fg_oc_matrices",
+    "fg_oc_matrices_workspace_size", "fg_oc_matrices", "fg_brute_knn",
 )
 
 _P = ctypes.c_void_p
@@ -73,6 +73,8 @@ _SIGS = {
     "fg_oc_matrices_workspace_size": ([_I64, _I64, _SZ], ctypes.c_int),
     "fg_oc_matrices": ([_P, _P, _I32, _P, _P, _I64, _I64, _I64, _I64, _P, _P, _P, _P,
                         ctypes.c_size_t, _P], ctypes.c_int),
+    "fg_brute_knn": ([_P, _I64, _I32, _P, _I32, _P, _I64, _P, _D, _U32, _I32, _P, _P, _P],
+                     ctypes.c_int),
     "fg_error_string": ([ctypes.c_int], ctypes.c_char_p),
     "fg_abi_version": ([], ctypes.c_int),
     "fg_launch_count": ([], ctypes.c_uint64),

@@ -110,10 +110,20 @@ def binned_knn(coords, bin_idx, sort_order, bin_bounds, bin_counts, min_widths, 
 
 def brute_knn(coords, offsets, dir_mask, use_dir, max_r2, use_max_r2, k, out_idx, out_d2,
               threads):
-    """pyx:394-409: one cell per split -> every split member is a candidate."""
+    """pyx:394-409 on the brute-force kernel (csrc/fg_verify.cu)."""
     del threads
-    _run_search(_upload_coords(coords), offsets, 1, 1, dir_mask, use_dir, max_r2, use_max_r2,
-                False, k, out_idx, out_d2)
+    c = _upload_coords(coords)
+    rs = torch.from_numpy(np.ascontiguousarray(offsets, dtype=np.int64)).to(c.device)
+    direction = None
+    if use_dir:
+        direction = torch.from_numpy(np.ascontiguousarray(dir_mask, dtype=np.int8)).to(c.device)
+    if int(k) > 128:  # beyond the verifier kernel's list: the binned search on one cell per split
+        _run_search(c, offsets, 1, 1, dir_mask, use_dir, max_r2, use_max_r2, False, k, out_idx,
+                    out_d2)
+        return
+    idx, d2 = ops.brute_knn(c, rs, int(k), None, direction, float(max_r2) if use_max_r2 else None)
+    out_idx[...] = idx.cpu().numpy()
+    out_d2[...] = d2.cpu().numpy()
 
 
 def install(gridknn_module) -> None:

@@ -88,11 +88,15 @@ def binned_select_knn(cloud: PointCloud, index: BinIndex, opts: KnnOptions, *,
 
 
 def brute_force_knn(cloud: PointCloud, opts: KnnOptions, *, d2_f64: bool = False) -> NeighborMatrix:
-    """Every vertex of the split is a candidate (G/knn.py:118-132): the same
-    kernel over a one-cell-per-split grid (n_bins = 1)."""
+    """Every vertex of the split is a candidate (G/knn.py:118-132): the
+    brute-force kernel (csrc/fg_verify.cu), independent of the binned search;
+    canonical (d2, index) rows, float64 distances (rounded to float32 unless
+    ``d2_f64``)."""
     _check_options(cloud, opts)
-    index = build_bin_index(cloud, BinningConfig(k_target=int(opts.k)), d_bin=1, n_bins=1)
-    return _search(cloud, index, opts, False, d2_f64)
+    rs = cloud.row_splits.device_tensor(cloud.coords.device)
+    idx, d2 = ops.brute_knn(cloud.coords.detach(), rs, int(opts.k), None, _direction(cloud, opts),
+                            None if opts.max_radius2 is None else float(opts.max_radius2))
+    return NeighborMatrix(idx, d2 if d2_f64 else d2.to(torch.float32))
 
 
 def knn_backward(cloud: PointCloud, neighbors: NeighborMatrix, upstream) -> torch.Tensor:

@@ -391,6 +391,45 @@ def _kg_backward(ctx, grad_idx, grad_d2, grad_agg):
 knn_gravnet.register_autograd(_kg_backward, setup_context=_kg_setup)
 
 
+# ---------------------------------------------------------------- brute force (verifier)
+@torch.library.custom_op(f"{_LIB_NS}::brute_knn", mutates_args=())
+def brute_knn(coords: Tensor, row_splits: Tensor, K: int, queries: Optional[Tensor] = None,
+              direction: Optional[Tensor] = None,
+              max_radius2: Optional[float] = None) -> tuple[Tensor, Tensor]:
+    """Brute-force exact kNN (pyx:335-409, G/knn.py:118-132) with its own
+    kernel (csrc/fg_verify.cu, no code shared with the binned search): ->
+    (idx i32 [Q, K], d2 f64 [Q, K]) for the rows ``queries`` (default all),
+    canonical (d2, index) order."""
+    _require_cuda(coords)
+    L = _lib.load()
+    dev = coords.device
+    n, n_c = coords.shape
+    c = coords.to(torch.float32).contiguous()
+    rs = row_splits.to(device=dev, dtype=torch.int64).contiguous()
+    q = None if queries is None else queries.to(device=dev, dtype=torch.int32).contiguous()
+    nq = n if q is None else q.numel()
+    flags = 0
+    dr = None
+    if direction is not None:
+        flags |= _lib.FG_KNN_USE_DIRECTION
+        dr = direction.to(device=dev, dtype=torch.int8).contiguous()
+    if max_radius2 is not None:
+        flags |= _lib.FG_KNN_USE_MAX_R2
+    idx = torch.empty((nq, K), dtype=torch.int32, device=dev)
+    d2 = torch.empty((nq, K), dtype=torch.float64, device=dev)
+    _lib.check(L.fg_brute_knn(_p(c), n, n_c, _p(rs), rs.numel() - 1, _p(q), nq, _p(dr),
+                              float(max_radius2 or 0.0), flags, K, _p(idx), _p(d2), _stream(c)),
+               "brute_knn")
+    return idx, d2
+
+
+@brute_knn.register_fake
+def _brute_fake(coords, row_splits, K, queries=None, direction=None, max_radius2=None):
+    nq = coords.shape[0] if queries is None else queries.shape[0]
+    return (coords.new_empty((nq, K), dtype=torch.int32),
+            coords.new_empty((nq, K), dtype=torch.float64))
+
+
 # ---------------------------------------------------------------- association matrices
 # Object counts are data dependent (the result size is read back once), so these
 # two are plain functions over the C ABI rather than traceable torch.library ops.
