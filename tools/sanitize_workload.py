@@ -1,0 +1,77 @@
+"""Small workload for compute-sanitizer (memcheck / racecheck / synccheck /
+initcheck): every kernel family of the library on inputs small enough for the
+tools' 10-100x slowdown.  Run through tools/sanitize.sh; no oracle involved
+(correctness is the parity tests' job, this only exercises the code paths).
+
+Paths covered: binning (K1-K4), tile search (scan + finish + redo), the
+warp-per-query kernel (float64 output, direction mask, max_radius2,
+exhaustive, d = 10 with d_bin = 5), the clustered-data decline path, both
+backward modes (atomic, deterministic), GravNet forward/backward, the brute
+verifier, index_replacer, association matrices.
+"""
+
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2511_10442_b200 as fg  # noqa: E402
+from paper_2511_10442_b200 import ops  # noqa: E402
+from paper_2511_10442_b200.datasets import generate_associations, generate_dataset  # noqa: E402
+
+
+def run(coords, off, k, d_bin, **kw):
+    dev = torch.device("cuda", 0)
+    c = torch.from_numpy(coords.astype(np.float32)).to(dev)
+    rs = torch.from_numpy(off.astype(np.int64)).to(dev)
+    n_bins = fg.compute_n_bins(int(np.diff(off).max()), k, d_bin)
+    bi, so, bb, mins, widths, sc = ops.bin_by_coordinates(c, rs, d_bin, n_bins)
+    idx, d2 = ops.binned_select_knn(c, rs, bi, so, bb, mins, widths, sc, k, d_bin, n_bins,
+                                    kw.get("direction"), kw.get("max_r2"), kw.get("exhaustive", False),
+                                    kw.get("f64", False))
+    up = torch.randn(idx.shape, device=dev)
+    g1 = ops.binned_select_knn_grad(up, idx, c)
+    g2 = ops.binned_select_knn_grad(up, idx, c, None, True)
+    torch.cuda.synchronize()
+    return c, rs, idx, d2
+
+
+def main():
+    torch.manual_seed(0)
+    rng = np.random.default_rng(1)
+    dev = torch.device("cuda", 0)
+    # tile path (uniform, d = 4, k = 16), two splits
+    x, _ = generate_dataset(6000, 4, splits=2, seed=3)
+    off = np.array([0, 2500, 6000], np.int64)
+    c, rs, idx, d2 = run(x, off, 16, 4)
+    # GravNet on the tile-path rows
+    feats = torch.randn(6000, 8, device=dev, requires_grad=True)
+    d2r = d2.clone().requires_grad_(True)
+    agg = ops.gravnet_aggregate(feats, idx, d2r, 10.0, [0, 1], True)
+    agg.sum().backward()
+    # warp-per-query kernel: float64 output, mask, radius, exhaustive
+    direction = torch.from_numpy(rng.integers(0, 4, 6000).astype(np.int8)).to(dev)
+    run(x, off, 16, 4, f64=True, direction=direction)
+    run(x, off, 16, 4, max_r2=0.01)
+    run(x, off, 9, 4, exhaustive=True)
+    # d = 10, d_bin = 5 (config C shape), k = 64
+    x10, _ = generate_dataset(4000, 10, splits=1, seed=4)
+    run(x10, np.array([0, 4000], np.int64), 64, 5)
+    # clustered data: the tile kernels decline, warp-per-query takes every query
+    xc, _ = generate_dataset(5000, 4, splits=1, seed=2, distribution="clusters")
+    run(xc, np.array([0, 5000], np.int64), 40, 4)
+    # brute-force verifier and index_replacer
+    ops.brute_knn(c, rs, 16)
+    lut = torch.arange(6000, device=dev, dtype=torch.int32).flip(0).contiguous()
+    ops.index_replacer(idx.clone(), lut)
+    # association matrices
+    asso, aoff = generate_associations(3000, 2, 6, 7, 0.2)
+    fg.oc_helper(fg.Associations(asso, fg.RowSplits(aoff)))
+    torch.cuda.synchronize()
+    print("sanitize workload done")
+
+
+if __name__ == "__main__":
+    main()
