@@ -63,6 +63,7 @@ enum fg_status {
 #define FG_KNN_STATS 0x100       /* diagnostics: count search events (fg_knn_stats)        */
 #define FG_KNN_NO_TILE 0x200     /* diagnostics: skip the lane-per-query tile path         */
 #define FG_KNN_FUSED_EPI 0x800   /* diagnostics: tile epilogue inside the scan kernel      */
+#define FG_KNN_NO_HD 0x1000      /* diagnostics: skip the high-dimensional tile path       */
 
 /* Reducer codes for the GravNet aggregation (G/gravnet.py:26, order = blocks). */
 #define FG_REDUCE_MEAN 0
@@ -92,6 +93,17 @@ int fg_bin_by_coordinates(const float *coords, int64_t n, int32_t n_coords,
                           int32_t *bin_bounds, double *dim_mins, double *widths,
                           float *sorted_coords, void *workspace, size_t workspace_bytes,
                           void *stream);
+
+/* bin_by_coordinates on float64 coordinates (the reference's own dtype,
+ * G/core.py:129): bounding boxes and cells from the float64 values, so every
+ * array equals the reference's bit for bit for any finite input;
+ * sorted_coords holds the float32 rounding (the search's filter stream). */
+int fg_bin_by_coordinates_f64(const double *coords, int64_t n, int32_t n_coords,
+                              const int64_t *row_splits, int32_t n_splits, int32_t d_bin,
+                              int32_t n_bins, int64_t *bin_idx, int32_t *sort_order,
+                              int32_t *bin_bounds, double *dim_mins, double *widths,
+                              float *sorted_coords, void *workspace, size_t workspace_bytes,
+                              void *stream);
 
 /* index_replacer: io[i] = lut[io[i]] for io[i] >= 0, negatives kept.  The
  * reference does this implicitly (u = sort_order[p], pyx:262); fg_knn_fwd
@@ -128,6 +140,25 @@ int fg_knn_fwd_ws(const float *sorted_coords, const int32_t *sort_order, const i
                   double max_radius2, uint32_t flags, int32_t *out_idx, void *out_d2,
                   void *workspace, size_t workspace_bytes, void *stream);
 
+/* binned_select_knn forward on float64 coordinates (the reference's dtype):
+ * exact float64 keys from `coords` (n x n_coords, original order) in the
+ * reference's operation order, so indices AND float64 distances equal the
+ * reference's for any finite input; the float32 `sorted_coords` of
+ * fg_bin_by_coordinates_f64 drive a filter whose error bound is derived from
+ * max |coords| on the device.  Runs the lane-per-query tile kernel for every
+ * shape; k <= 64 and n_bins <= 32 (FG_ERR_UNSUPPORTED otherwise).  Same flags,
+ * outputs and canonical order as fg_knn_fwd_ws; FG_KNN_EXHAUSTIVE is accepted
+ * and changes nothing (same answer). */
+int fg_knn_f64_workspace_size(int64_t n, int32_t n_coords, int32_t n_splits, int32_t d_bin,
+                              int32_t n_bins, int32_t k, uint32_t flags, size_t *bytes);
+int fg_knn_fwd_f64_ws(const double *coords, const float *sorted_coords, const int32_t *sort_order,
+                      const int64_t *bin_idx, const int32_t *bin_bounds,
+                      const int64_t *row_splits, const double *dim_mins, const double *widths,
+                      int64_t n, int32_t n_coords, int32_t n_splits, int32_t d_bin,
+                      int32_t n_bins, int32_t k, const int8_t *dir_mask, double max_radius2,
+                      uint32_t flags, int32_t *out_idx, void *out_d2, void *workspace,
+                      size_t workspace_bytes, void *stream);
+
 /* Diagnostics: copy (and optionally reset) the counters accumulated by
  * fg_knn_fwd launches made with FG_KNN_STATS: warp-per-query kernel [queries,
  * regions, chunks, appends, compactions, speculative-radius failures, exact
@@ -147,6 +178,11 @@ int fg_brute_knn(const float *coords, int64_t n, int32_t n_coords, const int64_t
                  int32_t n_splits, const int32_t *queries, int64_t n_queries,
                  const int8_t *dir_mask, double max_radius2, uint32_t flags, int32_t k,
                  int32_t *out_idx, double *out_d2, void *stream);
+/* fg_brute_knn on float64 coordinates (the reference's dtype): same rows. */
+int fg_brute_knn_f64(const double *coords, int64_t n, int32_t n_coords, const int64_t *row_splits,
+                     int32_t n_splits, const int32_t *queries, int64_t n_queries,
+                     const int8_t *dir_mask, double max_radius2, uint32_t flags, int32_t k,
+                     int32_t *out_idx, double *out_d2, void *stream);
 
 /* ---------------------------------------------------------------- backward */
 
@@ -164,15 +200,18 @@ int fg_knn_bwd_workspace_size(int64_t n, int32_t n_coords, int32_t k, size_t *by
  *    fixed point (order-independent), ~2^-42 of the bucket's largest term:
  *    bitwise repeatable run to run like the reference's fixed-order np.add.at
  *    (pkg/tests/test_knn.py:302-309).
- * grad_d2 is float32 (a float64 upstream is rounded to float32 by the torch
- * op).  grad_coords is float32 (or double with FG_BWD_F64).  `order`
- * (nullable) is the row visiting order, e.g. the sort_order of
- * fg_bin_by_coordinates (spatial locality).
+ * coords and grad_d2 are float32, or double with FG_BWD_X64 / FG_BWD_G64
+ * (the reference's dtypes: terms 2g(x_v - x_u) in float64 exactly as numpy
+ * forms them; default path only).  grad_coords is float32 (or double with
+ * FG_BWD_F64).  `order` (nullable) is the row visiting order, e.g. the
+ * sort_order of fg_bin_by_coordinates (spatial locality).
  * Workspace from fg_knn_bwd_workspace_size(n, n_coords, k). */
 #define FG_BWD_F64 0x1
 #define FG_BWD_DETERMINISTIC 0x2
-int fg_knn_bwd(const float *coords, int64_t n, int32_t n_coords, const int32_t *idx, int32_t k,
-               const float *grad_d2, const int32_t *order, void *grad_coords, int32_t grad_flags,
+#define FG_BWD_X64 0x4 /* coords is double */
+#define FG_BWD_G64 0x8 /* grad_d2 is double */
+int fg_knn_bwd(const void *coords, int64_t n, int32_t n_coords, const int32_t *idx, int32_t k,
+               const void *grad_d2, const int32_t *order, void *grad_coords, int32_t grad_flags,
                void *workspace, size_t workspace_bytes, void *stream);
 
 /* ---------------------------------------------------------------- GravNet */

@@ -24,8 +24,11 @@ FG_KNN_D2_F64 = 0x8
 FG_KNN_STATS = 0x100
 FG_KNN_NO_TILE = 0x200
 FG_KNN_FUSED_EPI = 0x800
+FG_KNN_NO_HD = 0x1000
 FG_BWD_F64 = 0x1
 FG_BWD_DETERMINISTIC = 0x2
+FG_BWD_X64 = 0x4
+FG_BWD_G64 = 0x8
 FG_REDUCE_MEAN = 0
 FG_REDUCE_MAX = 1
 
@@ -37,6 +40,8 @@ EXPORTS = (
     "fg_launch_count", "fg_knn_stats", "fg_knn_workspace_size", "fg_knn_fwd_ws",
     "fg_knn_gravnet_fwd_ws", "fg_oc_unique_workspace_size", "fg_oc_find_unique",
     "fg_oc_matrices_workspace_size", "fg_oc_matrices", "fg_brute_knn",
+    "fg_bin_by_coordinates_f64", "fg_knn_f64_workspace_size", "fg_knn_fwd_f64_ws",
+    "fg_brute_knn_f64",
 )
 
 _P = ctypes.c_void_p
@@ -50,6 +55,11 @@ _SIGS = {
     "fg_bin_workspace_size": ([_I64, _I32, _I32, _I32, _SZ], ctypes.c_int),
     "fg_bin_by_coordinates": ([_P, _I64, _I32, _P, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P,
                                ctypes.c_size_t, _P], ctypes.c_int),
+    "fg_bin_by_coordinates_f64": ([_P, _I64, _I32, _P, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P,
+                                   _P, ctypes.c_size_t, _P], ctypes.c_int),
+    "fg_knn_f64_workspace_size": ([_I64, _I32, _I32, _I32, _I32, _I32, _U32, _SZ], ctypes.c_int),
+    "fg_knn_fwd_f64_ws": ([_P, _P, _P, _P, _P, _P, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _P,
+                           _D, _U32, _P, _P, _P, ctypes.c_size_t, _P], ctypes.c_int),
     "fg_index_replacer": ([_P, _I64, _P, _I64, _P], ctypes.c_int),
     "fg_knn_fwd": ([_P, _P, _P, _P, _P, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _P, _D, _U32,
                     _P, _P, _P], ctypes.c_int),
@@ -73,6 +83,8 @@ _SIGS = {
     "fg_oc_matrices_workspace_size": ([_I64, _I64, _SZ], ctypes.c_int),
     "fg_oc_matrices": ([_P, _P, _I32, _P, _P, _I64, _I64, _I64, _I64, _P, _P, _P, _P,
                         ctypes.c_size_t, _P], ctypes.c_int),
+    "fg_brute_knn_f64": ([_P, _I64, _I32, _P, _I32, _P, _I64, _P, _D, _U32, _I32, _P, _P, _P],
+                         ctypes.c_int),
     "fg_brute_knn": ([_P, _I64, _I32, _P, _I32, _P, _I64, _P, _D, _U32, _I32, _P, _P, _P],
                      ctypes.c_int),
     "fg_error_string": ([ctypes.c_int], ctypes.c_char_p),

@@ -14,12 +14,16 @@ makes an unmodified gridknn front-end route ``backend="cuda"`` here:
     idx = gridknn.build_bin_index(cloud, cfg, backend="cuda")
     nm = gridknn.binned_select_knn(cloud, idx, opts, backend="cuda")
 
-Differences a caller can observe (all within the reference's contract):
-rows come back sorted by (d2, index) with ties to the lower index (the
-reference leaves slot order unspecified, G/core.py:163-166); coordinates are
-processed as float32 on the device, so results are exact for
-float32-representable inputs (float64 distances are then bit-identical).
-The host copies make this a parity tool; timing goes through the torch ops.
+Coordinates stay float64 on the device: the bin index is built from the
+float64 values (bit-identical arrays) and the search ranks exact float64 keys
+computed from them in the reference's operation order (fg_knn_fwd_f64_ws), so
+indices and float64 distances equal the reference's for any finite input.
+Differences a caller can observe (all within the reference's contract): rows
+come back sorted by (d2, index) with ties to the lower index (the reference
+leaves slot order unspecified, G/core.py:163-166); ``binned_knn`` on float64
+coordinates takes k <= 64 and n_bins <= 32 (the tile kernel's buffers;
+BackendUnavailableError beyond).  The host copies make this a parity tool;
+timing goes through the torch ops.
 """
 
 from __future__ import annotations
@@ -38,7 +42,7 @@ def _dev():
 
 def _upload_coords(coords) -> torch.Tensor:
     c = np.ascontiguousarray(coords, dtype=np.float64)
-    return torch.from_numpy(c.astype(np.float32)).to(_dev())
+    return torch.from_numpy(c.copy()).to(_dev())
 
 
 def build_index(coords, offsets, d_bin, n_bins):

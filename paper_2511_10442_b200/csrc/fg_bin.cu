@@ -31,7 +31,7 @@ constexpr int kSmallCell = 32;
 constexpr int kMediumCell = 4096;
 
 struct BinWs {
-    unsigned* bbox;          // n_splits * d_bin * 2 (ordered min, ordered max)
+    unsigned long long* bbox;  // n_splits * d_bin * 2 (ordered-double min, max)
     int32_t* cursor;         // n_cells (histogram, then scatter cursor)
     unsigned long long* st;  // scan tile status words
     unsigned* counters;      // [0] scan tile ticket, [1] medium count, [2] big count
@@ -52,7 +52,7 @@ size_t carve(BinWs* w, void* base, int64_t n, int32_t n_splits, int32_t d_bin, i
     };
     w->n_tiles = ceil_div(n_cells, kScanTile);
     w->list_cap = n / (kSmallCell + 1) + 1;
-    w->bbox = (unsigned*)take(sizeof(unsigned) * (size_t)n_splits * d_bin * 2);
+    w->bbox = (unsigned long long*)take(sizeof(unsigned long long) * (size_t)n_splits * d_bin * 2);
     w->cursor = (int32_t*)take(sizeof(int32_t) * (size_t)n_cells);
     w->st = (unsigned long long*)take(sizeof(unsigned long long) * (size_t)w->n_tiles);
     w->counters = (unsigned*)take(sizeof(unsigned) * 4);
@@ -62,17 +62,28 @@ size_t carve(BinWs* w, void* base, int64_t n, int32_t n_splits, int32_t d_bin, i
 }
 
 // ---------------------------------------------------------------- K1
-__global__ void k_bbox_init(unsigned* bbox, int64_t m) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
-         i += (int64_t)gridDim.x * blockDim.x)
-        bbox[i] = (i & 1) ? 0u : 0xffffffffu;  // even = min slot, odd = max slot
+// Order-preserving double <-> uint64 map (the bbox atomics; float input is
+// widened exactly, so one map serves both coordinate types).
+__device__ __forceinline__ unsigned long long double_to_ordered(double f) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(f);
+    return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double ordered_to_double(unsigned long long u) {
+    const unsigned long long b = (u & 0x8000000000000000ull) ? (u & 0x7fffffffffffffffull) : ~u;
+    return __longlong_as_double((long long)b);
 }
 
-template <int DB>
-__global__ void __launch_bounds__(256) k_bbox(const float* __restrict__ coords, int64_t n, int n_c,
+__global__ void k_bbox_init(unsigned long long* bbox, int64_t m) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x)
+        bbox[i] = (i & 1) ? 0ull : ~0ull;  // even = min slot, odd = max slot
+}
+
+template <typename T, int DB>
+__global__ void __launch_bounds__(256) k_bbox(const T* __restrict__ coords, int64_t n, int n_c,
                                               const int64_t* __restrict__ rs, int n_splits,
-                                              int64_t chunk, unsigned* __restrict__ bbox) {
-    __shared__ float s_mn[8][DB], s_mx[8][DB];
+                                              int64_t chunk, unsigned long long* __restrict__ bbox) {
+    __shared__ T s_mn[8][DB], s_mx[8][DB];
     int64_t lo = blockIdx.x * chunk;
     const int64_t hi = min(n, lo + chunk);
     if (lo >= hi) return;
@@ -83,26 +94,26 @@ __global__ void __launch_bounds__(256) k_bbox(const float* __restrict__ coords, 
             ++s;
             continue;
         }
-        float mn[DB], mx[DB];
+        T mn[DB], mx[DB];
 #pragma unroll
         for (int d = 0; d < DB; ++d) {
-            mn[d] = __int_as_float(0x7f800000);   // +inf
-            mx[d] = -__int_as_float(0x7f800000);  // -inf
+            mn[d] = (T)__builtin_huge_val();
+            mx[d] = -(T)__builtin_huge_val();
         }
         for (int64_t v = lo + threadIdx.x; v < seg_end; v += blockDim.x) {
 #pragma unroll
             for (int d = 0; d < DB; ++d) {
-                const float x = coords[v * n_c + d];
-                mn[d] = fminf(mn[d], x);
-                mx[d] = fmaxf(mx[d], x);
+                const T x = coords[v * n_c + d];
+                mn[d] = min(mn[d], x);
+                mx[d] = max(mx[d], x);
             }
         }
 #pragma unroll
         for (int d = 0; d < DB; ++d) {
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
-                mn[d] = fminf(mn[d], __shfl_xor_sync(FG_FULL_MASK, mn[d], o));
-                mx[d] = fmaxf(mx[d], __shfl_xor_sync(FG_FULL_MASK, mx[d], o));
+                mn[d] = min(mn[d], __shfl_xor_sync(FG_FULL_MASK, mn[d], o));
+                mx[d] = max(mx[d], __shfl_xor_sync(FG_FULL_MASK, mx[d], o));
             }
         }
         const int w = threadIdx.x >> 5;
@@ -116,13 +127,13 @@ __global__ void __launch_bounds__(256) k_bbox(const float* __restrict__ coords, 
         __syncthreads();
         if (threadIdx.x < DB) {
             const int d = threadIdx.x;
-            float a = s_mn[0][d], b = s_mx[0][d];
+            T a = s_mn[0][d], b = s_mx[0][d];
             for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
-                a = fminf(a, s_mn[i][d]);
-                b = fmaxf(b, s_mx[i][d]);
+                a = min(a, s_mn[i][d]);
+                b = max(b, s_mx[i][d]);
             }
-            atomicMin(&bbox[((int64_t)s * DB + d) * 2 + 0], float_to_ordered(a));
-            atomicMax(&bbox[((int64_t)s * DB + d) * 2 + 1], float_to_ordered(b));
+            atomicMin(&bbox[((int64_t)s * DB + d) * 2 + 0], double_to_ordered((double)a));
+            atomicMax(&bbox[((int64_t)s * DB + d) * 2 + 1], double_to_ordered((double)b));
         }
         __syncthreads();
         lo = seg_end;
@@ -131,7 +142,7 @@ __global__ void __launch_bounds__(256) k_bbox(const float* __restrict__ coords, 
 }
 
 // pyx:99-118: empty split keeps min 0 / width 1; width = ext / n_bins or 1.0.
-__global__ void k_bbox_final(const unsigned* __restrict__ bbox, const int64_t* __restrict__ rs,
+__global__ void k_bbox_final(const unsigned long long* __restrict__ bbox, const int64_t* __restrict__ rs,
                              int n_splits, int d_bin, int n_bins, double* __restrict__ mins,
                              double* __restrict__ widths) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -142,16 +153,16 @@ __global__ void k_bbox_final(const unsigned* __restrict__ bbox, const int64_t* _
         widths[i] = 1.0;
         return;
     }
-    const double mn = (double)ordered_to_float(bbox[i * 2 + 0]);
-    const double mx = (double)ordered_to_float(bbox[i * 2 + 1]);
+    const double mn = ordered_to_double(bbox[i * 2 + 0]);
+    const double mx = ordered_to_double(bbox[i * 2 + 1]);
     const double ext = __dsub_rn(mx, mn);
     mins[i] = mn;
     widths[i] = ext > 0.0 ? __ddiv_rn(ext, (double)n_bins) : 1.0;
 }
 
 // ---------------------------------------------------------------- K2
-template <int DB>
-__global__ void __launch_bounds__(256) k_assign(const float* __restrict__ coords, int64_t n, int n_c,
+template <typename T, int DB>
+__global__ void __launch_bounds__(256) k_assign(const T* __restrict__ coords, int64_t n, int n_c,
                                                 const int64_t* __restrict__ rs, int n_splits,
                                                 int n_bins, int64_t total,
                                                 const double* __restrict__ mins,
@@ -196,25 +207,25 @@ __global__ void __launch_bounds__(256) k_scatter(const int64_t* __restrict__ bin
     if (live) sort_order[base + __popc(peers & lanemask_lt())] = (int32_t)v;
 }
 
-template <int NV>
-__device__ __forceinline__ void gather_row(const float* __restrict__ coords, int n_c, int32_t v,
+template <int NV, typename T>
+__device__ __forceinline__ void gather_row(const T* __restrict__ coords, int n_c, int32_t v,
                                            float4* __restrict__ dst) {
-    const float* src = coords + (int64_t)v * n_c;
+    const T* src = coords + (int64_t)v * n_c;
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
         float t[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) t[e] = (4 * j + e < n_c) ? src[4 * j + e] : 0.0f;
+        for (int e = 0; e < 4; ++e) t[e] = (4 * j + e < n_c) ? (float)src[4 * j + e] : 0.0f;
         dst[j] = make_float4(t[0], t[1], t[2], t[3]);
     }
 }
 
 // Thread per cell: sort segments of <= 32 ids (insertion sort), gather coords;
 // longer segments are queued for the CTA-level fix-ups.
-template <int NV>
+template <int NV, typename T>
 __global__ void __launch_bounds__(256) k_fix_small(const int32_t* __restrict__ bounds, int64_t n_cells,
                                                    int32_t* __restrict__ sort_order,
-                                                   const float* __restrict__ coords, int n_c,
+                                                   const T* __restrict__ coords, int n_c,
                                                    float4* __restrict__ sorted,
                                                    unsigned* __restrict__ counters,
                                                    int32_t* __restrict__ medium,
@@ -247,10 +258,10 @@ __global__ void __launch_bounds__(256) k_fix_small(const int32_t* __restrict__ b
     }
 }
 
-template <int NV>
+template <int NV, typename T>
 __global__ void __launch_bounds__(1024) k_fix_medium(const int32_t* __restrict__ bounds,
                                                      int32_t* __restrict__ sort_order,
-                                                     const float* __restrict__ coords, int n_c,
+                                                     const T* __restrict__ coords, int n_c,
                                                      float4* __restrict__ sorted,
                                                      const unsigned* __restrict__ counters,
                                                      const int32_t* __restrict__ medium) {
@@ -288,12 +299,12 @@ __global__ void __launch_bounds__(1024) k_fix_medium(const int32_t* __restrict__
 // Huge cells: the members of cell c in ascending id order are exactly the
 // vertices v of its split with bin_idx[v] == c, so one CTA compacts the
 // split range in order (block-wide exclusive scan per chunk).
-template <int NV>
+template <int NV, typename T>
 __global__ void __launch_bounds__(1024) k_fix_big(const int32_t* __restrict__ bounds,
                                                   const int64_t* __restrict__ bin_idx,
                                                   const int64_t* __restrict__ rs, int64_t total,
                                                   int32_t* __restrict__ sort_order,
-                                                  const float* __restrict__ coords, int n_c,
+                                                  const T* __restrict__ coords, int n_c,
                                                   float4* __restrict__ sorted,
                                                   const unsigned* __restrict__ counters,
                                                   const int32_t* __restrict__ big) {
@@ -334,26 +345,26 @@ __global__ void __launch_bounds__(1024) k_fix_big(const int32_t* __restrict__ bo
     }
 }
 
-template <int NV>
+template <int NV, typename T>
 int launch_fixups(const int32_t* bounds, int64_t n_cells, int32_t* sort_order, const int64_t* bin_idx,
-                  const int64_t* rs, int64_t total, const float* coords, int n_c, float* sorted,
+                  const int64_t* rs, int64_t total, const T* coords, int n_c, float* sorted,
                   const BinWs& w, cudaStream_t st) {
     float4* s4 = reinterpret_cast<float4*>(sorted);
     if (n_cells > 0) {
-        k_fix_small<NV><<<(unsigned)ceil_div(n_cells, 256), 256, 0, st>>>(
+        k_fix_small<NV, T><<<(unsigned)ceil_div(n_cells, 256), 256, 0, st>>>(
             bounds, n_cells, sort_order, coords, n_c, s4, w.counters, w.medium, w.big);
         FG_TRY(launched(st));
     }
-    k_fix_medium<NV><<<296, 1024, 0, st>>>(bounds, sort_order, coords, n_c, s4, w.counters,
+    k_fix_medium<NV, T><<<296, 1024, 0, st>>>(bounds, sort_order, coords, n_c, s4, w.counters,
                                            w.medium);
     FG_TRY(launched(st));
-    k_fix_big<NV><<<148, 1024, 0, st>>>(bounds, bin_idx, rs, total, sort_order, coords, n_c, s4,
+    k_fix_big<NV, T><<<148, 1024, 0, st>>>(bounds, bin_idx, rs, total, sort_order, coords, n_c, s4,
                                         w.counters, w.big);
     return launched(st);
 }
 
-template <int DB>
-int launch_bin_core(const float* coords, int64_t n, int n_c, const int64_t* rs, int n_splits,
+template <typename T, int DB>
+int launch_bin_core(const T* coords, int64_t n, int n_c, const int64_t* rs, int n_splits,
                     int n_bins, int64_t total, double* mins, double* widths, int64_t* bin_idx,
                     const BinWs& w, cudaStream_t st) {
     const int64_t m = (int64_t)n_splits * DB * 2;
@@ -361,7 +372,7 @@ int launch_bin_core(const float* coords, int64_t n, int n_c, const int64_t* rs, 
     FG_TRY(launched(st));
     if (n > 0) {
         const int64_t chunk = 2048;
-        k_bbox<DB><<<(unsigned)ceil_div(n, chunk), 256, 0, st>>>(coords, n, n_c, rs, n_splits,
+        k_bbox<T, DB><<<(unsigned)ceil_div(n, chunk), 256, 0, st>>>(coords, n, n_c, rs, n_splits,
                                                                  chunk, w.bbox);
         FG_TRY(launched(st));
     }
@@ -369,7 +380,7 @@ int launch_bin_core(const float* coords, int64_t n, int n_c, const int64_t* rs, 
         w.bbox, rs, n_splits, DB, n_bins, mins, widths);
     FG_TRY(launched(st));
     if (n > 0) {
-        k_assign<DB><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
+        k_assign<T, DB><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
             coords, n, n_c, rs, n_splits, n_bins, total, mins, widths, bin_idx, w.cursor);
         FG_TRY(launched(st));
     }
@@ -394,12 +405,12 @@ extern "C" int fg_bin_workspace_size(int64_t n, int32_t n_splits, int32_t d_bin,
     return 0;
 }
 
-extern "C" int fg_bin_by_coordinates(const float* coords, int64_t n, int32_t n_coords,
-                                     const int64_t* row_splits, int32_t n_splits, int32_t d_bin,
-                                     int32_t n_bins, int64_t* bin_idx, int32_t* sort_order,
-                                     int32_t* bin_bounds, double* dim_mins, double* widths,
-                                     float* sorted_coords, void* workspace,
-                                     size_t workspace_bytes, void* stream) {
+namespace {
+template <typename T>
+int bin_entry(const T* coords, int64_t n, int32_t n_coords, const int64_t* row_splits,
+              int32_t n_splits, int32_t d_bin, int32_t n_bins, int64_t* bin_idx,
+              int32_t* sort_order, int32_t* bin_bounds, double* dim_mins, double* widths,
+              float* sorted_coords, void* workspace, size_t workspace_bytes, void* stream) {
     if (n < 0 || n >= ((int64_t)1 << 31) || n_splits < 1 || n_bins < 1) return FG_ERR_BAD_SHAPE;
     if (n_coords > 16) return FG_ERR_TOO_MANY_DIMS;
     if (d_bin < 1 || d_bin > kMaxBinDims || d_bin > n_coords) return FG_ERR_TOO_FEW_DIMS;
@@ -418,11 +429,11 @@ extern "C" int fg_bin_by_coordinates(const float* coords, int64_t n, int32_t n_c
     FG_CUDA(cudaMemsetAsync(w.counters, 0, sizeof(unsigned) * 4, st));
 
     switch (d_bin) {
-        case 1: FG_TRY(launch_bin_core<1>(coords, n, n_coords, row_splits, n_splits, n_bins, total, dim_mins, widths, bin_idx, w, st)); break;
-        case 2: FG_TRY(launch_bin_core<2>(coords, n, n_coords, row_splits, n_splits, n_bins, total, dim_mins, widths, bin_idx, w, st)); break;
-        case 3: FG_TRY(launch_bin_core<3>(coords, n, n_coords, row_splits, n_splits, n_bins, total, dim_mins, widths, bin_idx, w, st)); break;
-        case 4: FG_TRY(launch_bin_core<4>(coords, n, n_coords, row_splits, n_splits, n_bins, total, dim_mins, widths, bin_idx, w, st)); break;
-        default: FG_TRY(launch_bin_core<5>(coords, n, n_coords, row_splits, n_splits, n_bins, total, dim_mins, widths, bin_idx, w, st)); break;
+        case 1: FG_TRY((launch_bin_core<T, 1>(coords, n, n_coords, row_splits, n_splits, n_bins, total, dim_mins, widths, bin_idx, w, st))); break;
+        case 2: FG_TRY((launch_bin_core<T, 2>(coords, n, n_coords, row_splits, n_splits, n_bins, total, dim_mins, widths, bin_idx, w, st))); break;
+        case 3: FG_TRY((launch_bin_core<T, 3>(coords, n, n_coords, row_splits, n_splits, n_bins, total, dim_mins, widths, bin_idx, w, st))); break;
+        case 4: FG_TRY((launch_bin_core<T, 4>(coords, n, n_coords, row_splits, n_splits, n_bins, total, dim_mins, widths, bin_idx, w, st))); break;
+        default: FG_TRY((launch_bin_core<T, 5>(coords, n, n_coords, row_splits, n_splits, n_bins, total, dim_mins, widths, bin_idx, w, st))); break;
     }
     fg::k_scan<<<(unsigned)w.n_tiles, kScanThreads, 0, st>>>(w.cursor, n_cells, bin_bounds, w.cursor,
                                                         w.st, w.counters);
@@ -432,11 +443,34 @@ extern "C" int fg_bin_by_coordinates(const float* coords, int64_t n, int32_t n_c
     FG_TRY(launched(st));
     const int nv = (n_coords + 3) / 4;
     switch (nv) {
-        case 1: return launch_fixups<1>(bin_bounds, n_cells, sort_order, bin_idx, row_splits, total, coords, n_coords, sorted_coords, w, st);
-        case 2: return launch_fixups<2>(bin_bounds, n_cells, sort_order, bin_idx, row_splits, total, coords, n_coords, sorted_coords, w, st);
-        case 3: return launch_fixups<3>(bin_bounds, n_cells, sort_order, bin_idx, row_splits, total, coords, n_coords, sorted_coords, w, st);
-        default: return launch_fixups<4>(bin_bounds, n_cells, sort_order, bin_idx, row_splits, total, coords, n_coords, sorted_coords, w, st);
+        case 1: return launch_fixups<1, T>(bin_bounds, n_cells, sort_order, bin_idx, row_splits, total, coords, n_coords, sorted_coords, w, st);
+        case 2: return launch_fixups<2, T>(bin_bounds, n_cells, sort_order, bin_idx, row_splits, total, coords, n_coords, sorted_coords, w, st);
+        case 3: return launch_fixups<3, T>(bin_bounds, n_cells, sort_order, bin_idx, row_splits, total, coords, n_coords, sorted_coords, w, st);
+        default: return launch_fixups<4, T>(bin_bounds, n_cells, sort_order, bin_idx, row_splits, total, coords, n_coords, sorted_coords, w, st);
     }
+}
+}  // namespace
+
+extern "C" int fg_bin_by_coordinates(const float* coords, int64_t n, int32_t n_coords,
+                                     const int64_t* row_splits, int32_t n_splits, int32_t d_bin,
+                                     int32_t n_bins, int64_t* bin_idx, int32_t* sort_order,
+                                     int32_t* bin_bounds, double* dim_mins, double* widths,
+                                     float* sorted_coords, void* workspace,
+                                     size_t workspace_bytes, void* stream) {
+    return bin_entry<float>(coords, n, n_coords, row_splits, n_splits, d_bin, n_bins, bin_idx,
+                            sort_order, bin_bounds, dim_mins, widths, sorted_coords, workspace,
+                            workspace_bytes, stream);
+}
+
+extern "C" int fg_bin_by_coordinates_f64(const double* coords, int64_t n, int32_t n_coords,
+                                         const int64_t* row_splits, int32_t n_splits,
+                                         int32_t d_bin, int32_t n_bins, int64_t* bin_idx,
+                                         int32_t* sort_order, int32_t* bin_bounds,
+                                         double* dim_mins, double* widths, float* sorted_coords,
+                                         void* workspace, size_t workspace_bytes, void* stream) {
+    return bin_entry<double>(coords, n, n_coords, row_splits, n_splits, d_bin, n_bins, bin_idx,
+                             sort_order, bin_bounds, dim_mins, widths, sorted_coords, workspace,
+                             workspace_bytes, stream);
 }
 
 namespace fg {

@@ -71,10 +71,10 @@ __device__ __forceinline__ void two_sum_add(float4* hi_acc, float4* lo_acc, cons
 
 // Warp per row (visited in `order` when given: spatially sorted rows keep the
 // neighbour gathers and the atomic targets local), lanes over slots.
-template <int NV>
-__global__ void __launch_bounds__(kRowWarps * 32) k_knn_bwd(const float* __restrict__ coords, int64_t n,
+template <int NV, typename TC, typename TG>
+__global__ void __launch_bounds__(kRowWarps * 32) k_knn_bwd(const TC* __restrict__ coords, int64_t n,
                                                           int n_c, const int32_t* __restrict__ idx,
-                                                          int k, const float* __restrict__ gd2,
+                                                          int k, const TG* __restrict__ gd2,
                                                           const int32_t* __restrict__ order,
                                                           float4* __restrict__ hi,
                                                           float4* __restrict__ lo) {
@@ -101,7 +101,9 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_knn_bwd(const float* __restr
                 for (int e = 0; e < 4; ++e) {
                     const int i = 4 * j + e;
                     const double xu = i < n_c ? (double)coords[(int64_t)u * n_c + i] : 0.0;
-                    c[e] = two_g * (xv[i] - xu);  // exact: 24-bit g times a 25-bit difference
+                    // float32 inputs: exact (24-bit g times a 25-bit difference);
+                    // float64 inputs: numpy's (2g) * (x_v - x_u), G/knn.py:164-165
+                    c[e] = two_g * (xv[i] - xu);
                     qs[i] += c[e];
                     c[e] = -c[e];
                 }
@@ -775,10 +777,13 @@ extern "C" int fg_knn_bwd_workspace_size(int64_t n, int32_t n_coords, int32_t k,
     return 0;
 }
 
-extern "C" int fg_knn_bwd(const float* coords, int64_t n, int32_t n_coords, const int32_t* idx,
-                          int32_t k, const float* grad_d2, const int32_t* order, void* grad_coords,
+extern "C" int fg_knn_bwd(const void* coords_v, int64_t n, int32_t n_coords, const int32_t* idx,
+                          int32_t k, const void* grad_v, const int32_t* order, void* grad_coords,
                           int32_t grad_flags, void* workspace, size_t workspace_bytes,
                           void* stream) {
+    const bool x64 = grad_flags & FG_BWD_X64, g64 = grad_flags & FG_BWD_G64;
+    const float* coords = static_cast<const float*>(coords_v);
+    const float* grad_d2 = static_cast<const float*>(grad_v);
     const int grad_is_f64 = (grad_flags & FG_BWD_F64) ? 1 : 0;
     if (k < 1) return FG_ERR_BAD_K;
     if (n < 0 || n_coords < 1) return FG_ERR_BAD_SHAPE;
@@ -789,7 +794,7 @@ extern "C" int fg_knn_bwd(const float* coords, int64_t n, int32_t n_coords, cons
     const int nv = (n_coords + 3) / 4;
     const bt::Plan P = bt::plan(n, n_coords, k);
     if (grad_flags & FG_BWD_DETERMINISTIC) {
-        if (!P.ok) return FG_ERR_UNSUPPORTED;
+        if (!P.ok || x64 || g64) return FG_ERR_UNSUPPORTED;
         if (workspace_bytes < P.bytes) return FG_ERR_WORKSPACE;
         char* ws = static_cast<char*>(workspace);
         switch (nv) {
@@ -807,15 +812,32 @@ extern "C" int fg_knn_bwd(const float* coords, int64_t n, int32_t n_coords, cons
     FG_CUDA(cudaMemsetAsync(workspace, 0, 2 * half, st));
     const unsigned blocks = (unsigned)ceil_div(n, kRowWarps);
     const bool vec4 = n_coords == 4 && (reinterpret_cast<uintptr_t>(coords) & 15) == 0;
-    if (vec4 && k <= 33) {
+    if (x64 || g64) {
+        const double* c64 = static_cast<const double*>(coords_v);
+        const double* g64p = static_cast<const double*>(grad_v);
+#define FG_BWD_GEN(NVV)                                                                              \
+    if (x64 && g64)                                                                                  \
+        k_knn_bwd<NVV, double, double><<<blocks, kRowWarps * 32, 0, st>>>(c64, n, n_coords, idx, k, g64p, order, hi, lo); \
+    else if (x64)                                                                                    \
+        k_knn_bwd<NVV, double, float><<<blocks, kRowWarps * 32, 0, st>>>(c64, n, n_coords, idx, k, grad_d2, order, hi, lo); \
+    else                                                                                             \
+        k_knn_bwd<NVV, float, double><<<blocks, kRowWarps * 32, 0, st>>>(coords, n, n_coords, idx, k, g64p, order, hi, lo);
+        switch (nv) {
+            case 1: FG_BWD_GEN(1) break;
+            case 2: FG_BWD_GEN(2) break;
+            case 3: FG_BWD_GEN(3) break;
+            default: FG_BWD_GEN(4) break;
+        }
+#undef FG_BWD_GEN
+    } else if (vec4 && k <= 33) {
         k_knn_bwd_pipe<1, 1><<<blocks, kRowWarps * 32, 0, st>>>(coords, n, n_coords, idx, k, grad_d2, order, hi, lo);
     } else if (vec4 && k <= 65) {
         k_knn_bwd_pipe<1, 2><<<blocks, kRowWarps * 32, 0, st>>>(coords, n, n_coords, idx, k, grad_d2, order, hi, lo);
     } else switch (nv) {
-        case 1: k_knn_bwd<1><<<blocks, kRowWarps * 32, 0, st>>>(coords, n, n_coords, idx, k, grad_d2, order, hi, lo); break;
-        case 2: k_knn_bwd<2><<<blocks, kRowWarps * 32, 0, st>>>(coords, n, n_coords, idx, k, grad_d2, order, hi, lo); break;
-        case 3: k_knn_bwd<3><<<blocks, kRowWarps * 32, 0, st>>>(coords, n, n_coords, idx, k, grad_d2, order, hi, lo); break;
-        default: k_knn_bwd<4><<<blocks, kRowWarps * 32, 0, st>>>(coords, n, n_coords, idx, k, grad_d2, order, hi, lo); break;
+        case 1: k_knn_bwd<1, float, float><<<blocks, kRowWarps * 32, 0, st>>>(coords, n, n_coords, idx, k, grad_d2, order, hi, lo); break;
+        case 2: k_knn_bwd<2, float, float><<<blocks, kRowWarps * 32, 0, st>>>(coords, n, n_coords, idx, k, grad_d2, order, hi, lo); break;
+        case 3: k_knn_bwd<3, float, float><<<blocks, kRowWarps * 32, 0, st>>>(coords, n, n_coords, idx, k, grad_d2, order, hi, lo); break;
+        default: k_knn_bwd<4, float, float><<<blocks, kRowWarps * 32, 0, st>>>(coords, n, n_coords, idx, k, grad_d2, order, hi, lo); break;
     }
     FG_TRY(launched(st));
     const int64_t m = n * n_coords;

@@ -1,7 +1,7 @@
 // fg_knn.cu -- C ABI entry of binned_select_knn forward (kernels: fg_knn_impl.cuh).
 #include <mutex>
 
-#include "fg_knn_tile.cuh"
+#include "fg_knn_hd.cuh"
 
 using namespace fg;
 using namespace fg::search;
@@ -18,7 +18,7 @@ int reducer_bits(const int32_t* reducers, int n_red, unsigned* bits);
 namespace {
 unsigned long long* g_stats_dev = nullptr;  // FG_KNN_STATS counters (lazily allocated)
 std::mutex g_stats_mu;
-constexpr int kStatsTotal = ST_COUNT + tile::TS_COUNT;
+constexpr int kStatsTotal = ST_COUNT + tile::TS_COUNT + hd::HS_COUNT;
 
 // The lane-per-query tile path (fg_knn_tile.cuh) serves every coordinate
 // binned, d <= 4, k - 1 <= 40, no mask / radius / exhaustive / float64 output.
@@ -32,6 +32,22 @@ bool tile_path(int32_t n_coords, int32_t n_splits, int32_t d_bin, int32_t n_bins
     int64_t blocks = n_splits;  // lead blocks must fit the int32 tile descriptors
     for (int i = 0; i < d_bin - 1; ++i) blocks *= (n_bins + 1) / 2;
     return blocks < ((int64_t)1 << 30);
+}
+
+// The lane-per-query high-dimensional tile path (fg_knn_hd.cuh) serves what the
+// d <= 4 tile path does not: n_coords > 4 or d_bin < n_coords, k <= 64, no
+// mask / radius / exhaustive (float64 distances are fine).
+bool hd_shape(int32_t n_splits, int32_t d_bin, int32_t n_bins, int32_t k) {
+    if (!(n_bins <= 32 && k >= 1 && k <= hd::kMaxNeed1)) return false;
+    int64_t blocks = n_splits;
+    for (int i = 0; i < d_bin - 1; ++i) blocks *= (n_bins + 1) / 2;
+    return blocks < ((int64_t)1 << 30);
+}
+bool hd_path(int32_t n_coords, int32_t n_splits, int32_t d_bin, int32_t n_bins, int32_t k,
+             uint32_t flags) {
+    const uint32_t off = FG_KNN_EXHAUSTIVE | FG_KNN_NO_TILE | FG_KNN_NO_HD;
+    if (tile_path(n_coords, n_splits, d_bin, n_bins, k, flags)) return false;
+    return k >= 2 && !(flags & off) && hd_shape(n_splits, d_bin, n_bins, k);
 }
 
 // Argument validation shared by both entry points (before any CUDA call).
@@ -90,6 +106,24 @@ TileWs tile_ws(void* base, int64_t n, int32_t n_splits, int32_t d_bin, int32_t n
     w.bytes = off;
     return w;
 }
+TileWs hd_ws(void* base, int64_t n, int32_t n_splits, int32_t d_bin, int32_t n_bins) {
+    TileWs w{};
+    const int64_t nblk = (n_bins + 1) / 2;
+    int64_t bps = 1;
+    for (int i = 0; i < d_bin - 1; ++i) bps *= nblk;
+    w.n_blocks = bps * n_splits;
+    const int64_t max_tiles = n / 32 + w.n_blocks + 1;  // runs of 32 per block
+    char* p = static_cast<char*>(base);
+    size_t off = 0;
+    w.ctr = reinterpret_cast<int*>(p + off);
+    off += 64;
+    w.tiles = reinterpret_cast<int2*>(p + off);
+    off = align_up(off + sizeof(int2) * (size_t)max_tiles, 256);
+    w.redo = reinterpret_cast<int32_t*>(p + off);
+    off = align_up(off + sizeof(int32_t) * (size_t)std::max<int64_t>(n, 1), 256);
+    w.bytes = off;
+    return w;
+}
 }  // namespace
 
 extern "C" int fg_knn_workspace_size(int64_t n, int32_t n_coords, int32_t n_splits, int32_t d_bin,
@@ -98,7 +132,9 @@ extern "C" int fg_knn_workspace_size(int64_t n, int32_t n_coords, int32_t n_spli
     if (n < 0 || n_splits < 1 || n_bins < 1) return FG_ERR_BAD_SHAPE;
     *bytes = tile_path(n_coords, n_splits, d_bin, n_bins, k, flags)
                  ? tile_ws(nullptr, n, n_splits, d_bin, n_bins).bytes
-                 : 0;
+                 : hd_path(n_coords, n_splits, d_bin, n_bins, k, flags)
+                       ? hd_ws(nullptr, n, n_splits, d_bin, n_bins).bytes
+                       : 0;
     return 0;
 }
 
@@ -116,6 +152,8 @@ extern "C" int fg_knn_fwd(const float* sorted_coords, const int32_t* sort_order,
     size_t bytes = 0;
     if (tile_path(n_coords, n_splits, d_bin, n_bins, k, flags))
         bytes = tile_ws(nullptr, n, n_splits, d_bin, n_bins).bytes;
+    else if (hd_path(n_coords, n_splits, d_bin, n_bins, k, flags))
+        bytes = hd_ws(nullptr, n, n_splits, d_bin, n_bins).bytes;
     void* ws = nullptr;
     cudaStream_t st = (cudaStream_t)stream;
     if (bytes) FG_CUDA(cudaMallocAsync(&ws, bytes, st));
@@ -162,6 +200,8 @@ extern "C" int fg_knn_fwd_ws(const float* sorted_coords, const int32_t* sort_ord
     a.qlist = nullptr;
     a.qcount = nullptr;
     a.qall = nullptr;
+    a.x64 = nullptr;
+    a.rnd = nullptr;
     if (flags & FG_KNN_STATS) {
         std::lock_guard<std::mutex> lk(g_stats_mu);
         if (!g_stats_dev) {
@@ -199,11 +239,130 @@ extern "C" int fg_knn_fwd_ws(const float* sorted_coords, const int32_t* sort_ord
         t.stats = a.stats ? a.stats + ST_COUNT : nullptr;
         return tile::launch(t, a, d_bin, st);
     }
+    if (hd_path(n_coords, n_splits, d_bin, n_bins, k, flags)) {
+        const TileWs w = hd_ws(workspace, n, n_splits, d_bin, n_bins);
+        if (!workspace) return FG_ERR_NULL;
+        if (workspace_bytes < w.bytes) return FG_ERR_WORKSPACE;
+        tile::TileArgs t{};
+        t.sc = a.sc;
+        t.sid = sort_order;
+        t.bounds = bin_bounds;
+        t.mins = dim_mins;
+        t.widths = widths;
+        t.total = total;
+        t.nb = n_bins;
+        t.n = n;
+        t.k = k;
+        t.nblk = (n_bins + 1) / 2;
+        t.bps = (int)(w.n_blocks / n_splits);
+        t.n_blocks = (int)w.n_blocks;
+        t.tiles = w.tiles;
+        t.ctr = w.ctr;
+        t.redo = w.redo;
+        t.out_idx = out_idx;
+        t.stats = nullptr;
+        switch ((n_coords + 3) / 4) {
+            case 1: return hd::dispatch_hd_nv1(t, a, d_bin, st);
+            case 2: return hd::dispatch_hd_nv2(t, a, d_bin, st);
+            case 3: return hd::dispatch_hd_nv3(t, a, d_bin, st);
+            default: return hd::dispatch_hd_nv4(t, a, d_bin, st);
+        }
+    }
     switch ((n_coords + 3) / 4) {
         case 1: return dispatch_nv1(a, d_bin, st);
         case 2: return dispatch_nv2(a, d_bin, st);
         case 3: return dispatch_nv3(a, d_bin, st);
         default: return dispatch_nv4(a, d_bin, st);
+    }
+}
+
+extern "C" int fg_knn_f64_workspace_size(int64_t n, int32_t n_coords, int32_t n_splits,
+                                         int32_t d_bin, int32_t n_bins, int32_t k, uint32_t flags,
+                                         size_t* bytes) {
+    (void)n_coords;
+    (void)flags;
+    if (!bytes) return FG_ERR_NULL;
+    if (n < 0 || n_splits < 1 || n_bins < 1) return FG_ERR_BAD_SHAPE;
+    *bytes = hd_ws(nullptr, n, n_splits, d_bin, n_bins).bytes + 256;
+    return 0;
+}
+
+extern "C" int fg_knn_fwd_f64_ws(const double* coords, const float* sorted_coords,
+                                 const int32_t* sort_order, const int64_t* bin_idx,
+                                 const int32_t* bin_bounds, const int64_t* row_splits,
+                                 const double* dim_mins, const double* widths, int64_t n,
+                                 int32_t n_coords, int32_t n_splits, int32_t d_bin, int32_t n_bins,
+                                 int32_t k, const int8_t* dir_mask, double max_radius2,
+                                 uint32_t flags, int32_t* out_idx, void* out_d2, void* workspace,
+                                 size_t workspace_bytes, void* stream) {
+    FG_TRY(check_args(sorted_coords, sort_order, bin_idx, bin_bounds, row_splits, dim_mins, widths,
+                      n, n_coords, n_splits, d_bin, n_bins, k, dir_mask, max_radius2, flags,
+                      out_idx, out_d2));
+    if (n == 0) return 0;
+    if (!coords || !workspace) return FG_ERR_NULL;
+    if (!hd_shape(n_splits, d_bin, n_bins, k)) return FG_ERR_UNSUPPORTED;
+    const TileWs w = hd_ws(workspace, n, n_splits, d_bin, n_bins);
+    if (workspace_bytes < w.bytes + 256) return FG_ERR_WORKSPACE;
+    unsigned* rnd = reinterpret_cast<unsigned*>(static_cast<char*>(workspace) + w.bytes);
+    cudaStream_t st = (cudaStream_t)stream;
+    FG_CUDA(cudaMemsetAsync(rnd, 0, sizeof(unsigned), st));
+    const int64_t m = n * n_coords;
+    hd::k_abs_bound<<<(unsigned)std::min<int64_t>(ceil_div(m, 256), 148 * 8), 256, 0, st>>>(
+        coords, m, n_coords, rnd);
+    FG_TRY(launched(st));
+    int64_t total = 1;
+    for (int i = 0; i < d_bin; ++i) total *= n_bins;
+    KnnArgs a{};
+    a.sc = reinterpret_cast<const float4*>(sorted_coords);
+    a.sid = sort_order;
+    a.bin_idx = bin_idx;
+    a.bounds = bin_bounds;
+    a.rs = row_splits;
+    a.mins = dim_mins;
+    a.widths = widths;
+    a.n = n;
+    a.total = total;
+    a.n_c = n_coords;
+    a.n_splits = n_splits;
+    a.nb = n_bins;
+    a.k = k;
+    a.dir = dir_mask;
+    a.max_r2 = max_radius2;
+    a.flags = flags & ~(uint32_t)FG_KNN_EXHAUSTIVE;  // a diagnostic: same answer
+    a.out_idx = out_idx;
+    a.out_d2 = out_d2;
+    a.x64 = coords;
+    a.rnd = reinterpret_cast<const float*>(rnd);
+    if (flags & FG_KNN_STATS) {
+        std::lock_guard<std::mutex> lk(g_stats_mu);
+        if (!g_stats_dev) {
+            FG_CUDA(cudaMalloc(&g_stats_dev, sizeof(unsigned long long) * kStatsTotal));
+            FG_CUDA(cudaMemset(g_stats_dev, 0, sizeof(unsigned long long) * kStatsTotal));
+        }
+        a.stats = g_stats_dev;
+    }
+    tile::TileArgs t{};
+    t.sc = a.sc;
+    t.sid = sort_order;
+    t.bounds = bin_bounds;
+    t.mins = dim_mins;
+    t.widths = widths;
+    t.total = total;
+    t.nb = n_bins;
+    t.n = n;
+    t.k = k;
+    t.nblk = (n_bins + 1) / 2;
+    t.bps = (int)(w.n_blocks / n_splits);
+    t.n_blocks = (int)w.n_blocks;
+    t.tiles = w.tiles;
+    t.ctr = w.ctr;
+    t.redo = w.redo;
+    t.out_idx = out_idx;
+    switch ((n_coords + 3) / 4) {
+        case 1: return hd::dispatch_hd_nv1(t, a, d_bin, st);
+        case 2: return hd::dispatch_hd_nv2(t, a, d_bin, st);
+        case 3: return hd::dispatch_hd_nv3(t, a, d_bin, st);
+        default: return hd::dispatch_hd_nv4(t, a, d_bin, st);
     }
 }
 

@@ -1,0 +1,771 @@
+// fg_knn_hd.cuh -- binned_select_knn forward, lane-per-query tiles for the
+// cases the d <= 4 tile path does not take: more than 4 coordinates, or fewer
+// binned dims than coordinates (config C: 1M x 10, d_bin 5, k 64).  Replaces
+// pyx:188-329 for those shapes; same canonical answer.
+//
+// The warp-per-query kernel spends ~90 warp instructions per 32 candidates of
+// one query on region bookkeeping; at d = 10 a query scans ~10^5 candidates.
+// Here one warp owns a tile of 32 spatially compact queries (lane = query) and
+// every candidate is loaded once into shared memory and evaluated by all 32
+// lanes with packed fp32x2 arithmetic (FADD2 + FFMA2 over candidate pairs):
+// ~DE/2 + 1 warp instructions per candidate for 32 (query, candidate) pairs.
+//
+// * tiles (k_hd_tiles): the block of 2^(DB-1) lead rows x all last-dim cells
+//   (tile path blocks) is cut into runs of exactly 32 points in column-major
+//   (last-dim cell, lead row) order -- compact boxes, full warps.
+// * per tile: lane buffers of (fp32 d2, sorted position) in shared memory
+//   (kCap entries); a candidate enters lane l's buffer iff its fp32 d2 <=
+//   tau_l.  A full buffer is cut by a warp-cooperative radix select to the
+//   (need+1) smallest (self included) and tau_l drops to that value x (1+1e-5).
+// * region growth: stage radius rho; the region is every lead row whose box
+//   distance (binned dims) to the tile's query box is <= rho, trimmed along the
+//   last binned dim; stage i scans only the shell between the regions of rho_{i-1}
+//   and rho_i (recomputed with identical float operations, so no cell is scanned
+//   twice or skipped).  After a stage every lane's tau_l is tightened to its
+//   (need+1)-th smallest entry; the search stops when sqrt(max_l tau_l) <= rho:
+//   the binned distance never exceeds the full distance, so the region holds
+//   every point within each lane's tau_l.  rho_1 comes from the previous tile
+//   of the same warp (neighbouring tiles, similar radii).
+// * epilogue: lane j's buffer (self dropped) is handed to the warp-per-query
+//   kernel's exact epilogue (float64 keys in the reference's operation order,
+//   pyx:32-48; (d2_f64, index) order) one lane at a time.
+// * a lane whose buffer cannot be cut (>= kCap - 32 entries within 1e-5 of each
+//   other: duplicates) goes to the redo list of the warp-per-query kernel.
+#pragma once
+
+#include "fg_knn_tile.cuh"
+
+namespace fg {
+namespace hd {
+
+constexpr int kWarps = 2;      // warps per CTA
+constexpr int kCap = 96;       // per-lane buffer entries (need + 1 <= 64)
+constexpr int kStride = kCap + 1;
+constexpr int kMaxNeed1 = 64;  // host eligibility: k <= 64
+constexpr float kMargin = 1.0f + 1e-5f;
+constexpr float kTiny = 1e-35f;
+constexpr float kSlackCells = 1e-4f;
+constexpr float kInf = __builtin_huge_valf();
+
+enum { HS_TILES, HS_CHUNKS, HS_STAGES, HS_REDO, HS_COMPACT, HS_COUNT };  // HS_REDO: unused (no redo)
+
+template <int DE>
+struct HdWarp {
+    float bd[32 * kStride];    // lane buffers: fp32 d2 (odd stride: appends spread over banks)
+    int32_t bp[32 * kStride];  //               sorted positions
+    alignas(16) float sx[DE][32];  // one 32-candidate chunk, SoA
+    alignas(16) int32_t spos[32];
+    int32_t span_s[64], span_l[64];
+    search::WarpBuf<128> eb;   // epilogue scratch (the warp-per-query kernel's)
+};
+
+template <int DE>
+__host__ __device__ constexpr size_t hd_smem_bytes() {
+    return sizeof(HdWarp<DE>) * kWarps;
+}
+
+// ---------------------------------------------------------------- tile list
+// One warp per (split, lead block): lane c owns last-dim column c (nb <= 32);
+// the block's points in (column, row) order are cut into runs of 32.
+template <int DB>
+__global__ void __launch_bounds__(128) k_hd_tiles(const tile::TileArgs a) {
+    constexpr int NL = DB - 1;
+    const int lane = lane_id();
+    const int blk = blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (blk >= a.n_blocks) return;
+    const int s = blk / a.bps;
+    int o[NL > 0 ? NL : 1];
+    tile::block_origin<NL>(blk - s * a.bps, a.nblk, o);
+    const int nb = a.nb;
+    int col = 0;
+    if (lane < nb) {
+#pragma unroll
+        for (int r = 0; r < (1 << NL); ++r) {
+            int rowflat = 0;
+            bool ok = true;
+#pragma unroll
+            for (int i = 0; i < NL; ++i) {
+                const int j = o[i] + ((r >> (NL - 1 - i)) & 1);
+                ok &= j < nb;
+                rowflat = rowflat * nb + j;
+            }
+            if (ok) {
+                const int64_t rc = (int64_t)s * a.total + (int64_t)rowflat * nb + lane;
+                col += a.bounds[rc + 1] - a.bounds[rc];
+            }
+        }
+    }
+    const int T = __reduce_add_sync(FG_FULL_MASK, col);
+    const int nt = (T + 31) >> 5;
+    int t0 = 0;
+    if (lane == 0 && nt > 0) t0 = atomicAdd(&a.ctr[0], nt);
+    t0 = __shfl_sync(FG_FULL_MASK, t0, 0);
+    for (int i = lane; i < nt; i += 32) a.tiles[t0 + i] = make_int2(blk, 32 * i);
+}
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ unsigned long long dup2(float x) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(x));
+    return r;
+}
+
+// Region geometry of one stage: lead-dim enumeration box and the radius.
+template <int NL>
+struct Box {
+    int L[NL > 0 ? NL : 1], N[NL > 0 ? NL : 1];
+    float inv[NL > 0 ? NL : 1];
+    int rows;
+    float rho2;   // radius^2 (physical units); < 0: empty region
+    float slack;  // cell units
+};
+
+template <int DB>
+__device__ __forceinline__ Box<DB - 1> make_box(float rho2, const float (&lo)[DB], const float (&hi)[DB],
+                                               const float (&invw)[DB], int nb, float slack) {
+    constexpr int NL = DB - 1;
+    Box<NL> b;
+    b.rho2 = rho2;
+    b.slack = slack;
+    b.rows = rho2 < 0.0f ? 0 : 1;
+    const float rho = sqrtf(fmaxf(rho2, 0.0f)) * kMargin;
+#pragma unroll
+    for (int i = 0; i < NL; ++i) {
+        const float rc = rho * invw[i] + slack;
+        b.L[i] = (int)fmaxf(floorf(lo[i] - rc), 0.0f);
+        b.N[i] = max((int)fminf(floorf(hi[i] + rc), (float)(nb - 1)) - b.L[i] + 1, 0);
+        b.inv[i] = __frcp_rn((float)max(b.N[i], 1));
+        b.rows *= b.N[i];
+    }
+    return b;
+}
+
+// Last-dim cell piece [ca, cb] of lead row jd inside the stage's region
+// (ca > cb: empty).  Identical float operations for every caller.
+template <int DB>
+__device__ __forceinline__ void row_piece(const Box<DB - 1>& b, const int (&jd)[DB > 1 ? DB - 1 : 1],
+                                          const float (&lo)[DB], const float (&hi)[DB],
+                                          const float (&w)[DB], const float (&invw)[DB], int nb,
+                                          int& ca, int& cb) {
+    constexpr int NL = DB - 1;
+    ca = 1;
+    cb = 0;
+    if (b.rho2 < 0.0f) return;
+    bool inside = true;
+    float bd2 = 0.0f;
+#pragma unroll
+    for (int i = 0; i < NL; ++i) {
+        inside &= jd[i] >= b.L[i] && jd[i] < b.L[i] + b.N[i];
+        const float fj = (float)jd[i];
+        float g = fmaxf(fmaxf(fj - hi[i], lo[i] - (fj + 1.0f)) - b.slack, 0.0f) * w[i];
+        bd2 = fmaf(g, g, bd2);
+    }
+    const float rem = b.rho2 * (kMargin * kMargin) - bd2;
+    if (!inside || rem < 0.0f) return;
+    const float rc = sqrtf(rem) * invw[NL] * kMargin + b.slack;
+    ca = (int)fmaxf(floorf(lo[NL] - rc), 0.0f);
+    cb = (int)fminf(floorf(hi[NL] + rc), (float)(nb - 1));
+}
+
+// Exact float64 key of candidate cpos for the query (lane j's): the
+// reference's operation order (pyx:32-48) on the float64 coordinates in
+// float64 mode, on the float32 coordinates otherwise.
+template <int NV, bool X64>
+__device__ __forceinline__ double hd_key(const search::KnnArgs& a, const float (&qj)[4 * NV],
+                                         int32_t qid, int32_t cpos) {
+    if constexpr (X64) {
+        const double* x = a.x64 + (int64_t)qid * a.n_c;
+        const double* y = a.x64 + (int64_t)a.sid[cpos] * a.n_c;
+        double acc = 0.0;
+        for (int i = 0; i < a.n_c; ++i) {
+            const double t = __dsub_rn(x[i], y[i]);
+            acc = i == 0 ? __dmul_rn(t, t) : __dadd_rn(acc, __dmul_rn(t, t));
+        }
+        return acc;
+    } else {
+        float c[4 * NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            const float4 x = a.sc[(int64_t)cpos * NV + v];
+            c[4 * v] = x.x; c[4 * v + 1] = x.y; c[4 * v + 2] = x.z; c[4 * v + 3] = x.w;
+        }
+        return exact_d2<4 * NV>(qj, c, a.n_c);
+    }
+}
+
+// W.eb.p[0..m) -> (key, id, cp) with exact keys, sorted by (key, id); entries
+// beyond max_radius2 get the sentinel.  Returns the sorted length (pow2).
+template <int NV, bool X64, int DE>
+__device__ __noinline__ int exact_sort(HdWarp<DE>& W, const search::KnnArgs& a, int m,
+                                       const float (&qj)[4 * NV], int32_t qid) {
+    const int lane = lane_id();
+    const bool use_r2 = a.flags & FG_KNN_USE_MAX_R2;
+    int len = 32;
+    while (len < m) len <<= 1;
+    for (int e = lane; e < len; e += 32) {
+        unsigned long long key = ~0ull;
+        int32_t id = 0x7fffffff, cp = -1;
+        if (e < m) {
+            cp = W.eb.p[e];
+            const double d = hd_key<NV, X64>(a, qj, qid, cp);
+            if (!use_r2 || d <= a.max_r2) {
+                key = (unsigned long long)__double_as_longlong(d);
+                id = a.sid[cp];
+            }
+        }
+        W.eb.key[e] = key;
+        W.eb.id[e] = id;
+        W.eb.cp[e] = cp;
+    }
+    __syncwarp();
+    search::warp_sort_exact<128>(W.eb, len);
+    return len;
+}
+
+// fp32 filter bound of a true squared distance x in float64 mode: a candidate
+// whose float64 d2 is <= x has fp32 d2 (float32-rounded coordinates) <=
+// (sqrt(x) + r)^2, r = sqrt(n_c) x max |coordinate difference error|.
+__device__ __forceinline__ float up_bound(float x, float r) {
+    const float s = sqrtf(x) + r;
+    return s * s * kMargin + kTiny;
+}
+
+// Warp-cooperative cut of lane j's buffer to its keep smallest entries: exact
+// 32-bit radix select of the keep-th smallest fp32 d2 P; the true bound tt_j
+// becomes P (float64 mode: its upper bound) x (1+1e-5) and the filter
+// threshold tau_j follows; entries above tau_j are dropped.  When near-ties
+// leave no room (> kCap - 32 entries within the margin: duplicates), exactly
+// the keep smallest by (float64 key, index) are kept -- the canonical order.
+template <int NV, bool X64, int DE>
+__device__ __noinline__ int cut_lane(HdWarp<DE>& W, const search::KnnArgs& a, int j, int m, int keep,
+                                     float& tau_j, float& tt_j, const float (&qj)[4 * NV],
+                                     int32_t qid, float r) {
+    const int lane = lane_id();
+    constexpr int PER = kCap / 32;
+    float* bd = &W.bd[j * kStride];
+    int32_t* bp = &W.bp[j * kStride];
+    unsigned key[PER];
+    int32_t pv[PER];
+    unsigned lo_k = 0xffffffffu, hi_k = 0u;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int e = i * 32 + lane;
+        key[i] = e < m ? __float_as_uint(bd[e]) : 0xffffffffu;  // d2 >= 0: bits order like values
+        pv[i] = e < m ? bp[e] : 0;
+        if (e < m) {
+            lo_k = min(lo_k, key[i]);
+            hi_k = max(hi_k, key[i]);
+        }
+    }
+    lo_k = __reduce_min_sync(FG_FULL_MASK, lo_k);
+    hi_k = __reduce_max_sync(FG_FULL_MASK, hi_k);
+    const int nbits = 32 - __clz(lo_k ^ hi_k);
+    unsigned P = nbits >= 32 ? 0u : (lo_k & ~((1u << nbits) - 1u));
+#pragma unroll 1
+    for (int bit = nbits - 1; bit >= 0; --bit) {
+        const unsigned t = P | ((1u << bit) - 1u);
+        int c = 0;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) c += key[i] <= t ? 1 : 0;
+        c = __reduce_add_sync(FG_FULL_MASK, c);
+        if (c < keep) P |= 1u << bit;
+    }
+    // P = the keep-th smallest fp32 d2 exactly
+    const float Pf = __uint_as_float(P);
+    float tt = fminf(__shfl_sync(FG_FULL_MASK, tt_j, j), X64 ? up_bound(Pf, r) : Pf * kMargin + kTiny);
+    float nt = X64 ? up_bound(tt, r) : tt;
+    __syncwarp();
+    int kept = 0;
+#pragma unroll
+    for (int i = 0; i < PER; ++i)
+        kept += __popc(__ballot_sync(FG_FULL_MASK, (i * 32 + lane) < m && __uint_as_float(key[i]) <= nt));
+    int wpos = 0;
+    if (kept <= kCap - 32) {
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const bool k = (i * 32 + lane) < m && __uint_as_float(key[i]) <= nt;
+            const unsigned bal = __ballot_sync(FG_FULL_MASK, k);
+            if (k) {
+                const int pos = wpos + __popc(bal & lanemask_lt());
+                bd[pos] = __uint_as_float(key[i]);
+                bp[pos] = pv[i];
+            }
+            wpos += __popc(bal);
+        }
+    } else {  // near-ties: the keep smallest by (float64 key, index)
+#pragma unroll
+        for (int i = 0; i < PER; ++i)
+            if (i * 32 + lane < m) W.eb.p[i * 32 + lane] = pv[i];
+        __syncwarp();
+        exact_sort<NV, X64, DE>(W, a, m, qj, qid);
+        for (int e = lane; e < keep; e += 32) {  // valid keys sort first: a prefix
+            const unsigned long long kk = W.eb.key[e];
+            if (kk != ~0ull) {
+                bd[e] = __double2float_ru(__longlong_as_double((long long)kk));
+                bp[e] = W.eb.cp[e];
+            }
+        }
+        __syncwarp();
+        for (int e0 = 0; e0 < keep; e0 += 32)
+            wpos += __popc(__ballot_sync(FG_FULL_MASK, e0 + lane < keep && W.eb.key[e0 + lane] != ~0ull));
+        if (wpos >= keep) {
+            const float f = __double2float_ru(__longlong_as_double((long long)W.eb.key[keep - 1]));
+            tt = fminf(tt, f * kMargin + kTiny);
+            nt = X64 ? up_bound(tt, r) : tt;
+        }
+    }
+    __syncwarp();
+    if (lane == j) {
+        tau_j = nt;
+        tt_j = tt;
+    }
+    return wpos;
+}
+
+// Evaluate one 32-candidate chunk (W.sx / W.spos) against every lane's query
+// and append the passing entries to the lanes' buffers.
+template <int DE>
+__device__ __forceinline__ void eval_chunk(HdWarp<DE>& W, const unsigned long long (&qd)[DE], int nlive,
+                                           float tau, uint32_t bd_base, uint32_t bp_base, int& m) {
+    const uint32_t sx_addr = (uint32_t)__cvta_generic_to_shared(&W.sx[0][0]);
+    const uint32_t sp_addr = (uint32_t)__cvta_generic_to_shared(&W.spos[0]);
+#pragma unroll 2
+    for (int j = 0; j < 32; j += 4) {
+        if (j >= nlive) break;
+        unsigned long long acc0, acc1;
+#pragma unroll
+        for (int d = 0; d < DE; ++d) {
+            unsigned long long c0, c1, t0, t1;
+            asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(c0), "=l"(c1)
+                         : "r"(sx_addr + d * 128 + j * 4));
+            asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(t0) : "l"(qd[d]), "l"(c0));
+            asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(t1) : "l"(qd[d]), "l"(c1));
+            if (d == 0) {
+                asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(acc0) : "l"(t0));
+                asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(acc1) : "l"(t1));
+            } else {
+                asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(acc0) : "l"(t0), "l"(acc0));
+                asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(acc1) : "l"(t1), "l"(acc1));
+            }
+        }
+        float d0, d1, d2, d3;
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(acc0));
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(d2), "=f"(d3) : "l"(acc1));
+        const bool p0 = d0 <= tau, p1 = d1 <= tau, p2 = d2 <= tau, p3 = d3 <= tau;
+        if (__any_sync(FG_FULL_MASK, p0 | p1 | p2 | p3)) {
+            int4 cp;
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(cp.x), "=r"(cp.y), "=r"(cp.z), "=r"(cp.w) : "r"(sp_addr + j * 4));
+            const float dd[4] = {d0, d1, d2, d3};
+            const bool pp[4] = {p0, p1, p2, p3};
+            const int32_t cc[4] = {cp.x, cp.y, cp.z, cp.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (pp[u] && cc[u] >= 0) {
+                    asm volatile("st.shared.f32 [%0], %1;" ::"r"(bd_base + 4 * m), "f"(dd[u]));
+                    asm volatile("st.shared.b32 [%0], %1;" ::"r"(bp_base + 4 * m), "r"(cc[u]));
+                    ++m;
+                }
+            }
+        }
+    }
+}
+
+// Scan the given spans (one per lane) in 32-candidate chunks.
+template <int NV, int DE, bool X64>
+__device__ __forceinline__ void scan_spans(HdWarp<DE>& W, const search::KnnArgs& a, int32_t S, int32_t L,
+                                           const unsigned long long (&qd)[DE], float& tau, float& tt,
+                                           int& m, int keep, const float (&q)[4 * NV], int32_t qid,
+                                           float r, uint32_t bd_base, uint32_t bp_base,
+                                           unsigned long long& chunks, unsigned long long& cuts) {
+    const int lane = lane_id();
+    const unsigned nonempty = __ballot_sync(FG_FULL_MASK, L > 0);
+    if (!nonempty) return;
+    const bool use_dir = a.flags & FG_KNN_USE_DIRECTION;
+    const int ns = __popc(nonempty);
+    if (L > 0) {
+        const int dst = __popc(nonempty & lanemask_lt());
+        W.span_s[dst] = S;
+        W.span_l[dst] = L;
+    }
+    __syncwarp();
+    S = lane < ns ? W.span_s[lane] : 0;
+    L = lane < ns ? W.span_l[lane] : 0;
+    __syncwarp();
+    const int32_t incl = warp_inclusive_scan(L);
+    const int32_t excl = incl - L;
+    const int32_t T = __shfl_sync(FG_FULL_MASK, incl, 31);
+    const unsigned le = (2u << lane) - 1u;
+    for (int32_t f0 = 0; f0 < T; f0 += 32) {
+        ++chunks;
+        // make room: every lane may gain 32 entries in this chunk
+        unsigned full = __ballot_sync(FG_FULL_MASK, m > kCap - 32);
+        while (full) {
+            const int j = __ffs(full) - 1;
+            full &= full - 1;
+            ++cuts;
+            const int mj = __shfl_sync(FG_FULL_MASK, m, j);
+            float qj[4 * NV];
+#pragma unroll
+            for (int d = 0; d < 4 * NV; ++d) qj[d] = __shfl_sync(FG_FULL_MASK, q[d], j);
+            const int32_t qidj = __shfl_sync(FG_FULL_MASK, qid, j);
+            const int rr = cut_lane<NV, X64, DE>(W, a, j, mj, keep, tau, tt, qj, qidj, r);
+            if (lane == j) m = rr;
+        }
+        const int base = __popc(__ballot_sync(FG_FULL_MASK, lane < ns && incl <= f0));
+        const unsigned starts = __reduce_or_sync(
+            FG_FULL_MASK, (lane < ns && excl > f0 && excl < f0 + 32) ? 1u << (excl - f0) : 0u);
+        const int sidx = min(base + __popc(starts & le), 31);
+        const int32_t Ss = __shfl_sync(FG_FULL_MASK, S, sidx);
+        const int32_t Es = __shfl_sync(FG_FULL_MASK, excl, sidx);
+        const int32_t f = f0 + lane;
+        const int nlive = min(32, T - f0);
+        int32_t cpos = f < T ? Ss + (f - Es) : -1;
+        if (use_dir && cpos >= 0) {  // roles 1/2 are never candidates (pyx:265-266)
+            const int8_t role = a.dir[a.sid[cpos]];
+            if (role == 1 || role == 2) cpos = -1;
+        }
+        if (cpos >= 0) {
+            const float4* src = a.sc + (int64_t)cpos * NV;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                const float4 x = src[v];
+                if (4 * v + 0 < DE) W.sx[4 * v + 0][lane] = x.x;
+                if (4 * v + 1 < DE) W.sx[4 * v + 1][lane] = x.y;
+                if (4 * v + 2 < DE) W.sx[4 * v + 2][lane] = x.z;
+                if (4 * v + 3 < DE) W.sx[4 * v + 3][lane] = x.w;
+            }
+        } else {
+#pragma unroll
+            for (int d = 0; d < DE; ++d) W.sx[d][lane] = kInf;
+        }
+        W.spos[lane] = cpos;
+        __syncwarp();
+        eval_chunk<DE>(W, qd, nlive, tau, bd_base, bp_base, m);
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------- search
+template <int NV, int DB, int DE, bool X64>
+__global__ void __launch_bounds__(kWarps * 32) k_hd_search(const __grid_constant__ tile::TileArgs t,
+                                                           const __grid_constant__ search::KnnArgs a) {
+    constexpr int NL = DB - 1;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    HdWarp<DE>& W = reinterpret_cast<HdWarp<DE>*>(smem_raw)[threadIdx.x >> 5];
+    const int lane = lane_id();
+    const int nb = t.nb;
+    const int need = a.k - 1;
+    const int keep = need + 1;  // self stays in the buffer until the epilogue
+    const bool use_dir = a.flags & FG_KNN_USE_DIRECTION;
+    const bool use_r2 = a.flags & FG_KNN_USE_MAX_R2;
+    const float r = X64 ? *a.rnd : 0.0f;
+    // cell-unit slack: the float32 cell position of a float64 coordinate can be
+    // off by the rounding of the coordinate and of the split minimum
+    const uint32_t bd_base = (uint32_t)__cvta_generic_to_shared(&W.bd[lane * kStride]);
+    const uint32_t bp_base = (uint32_t)__cvta_generic_to_shared(&W.bp[lane * kStride]);
+    float rho2_hint = -1.0f;  // final radius^2 of this warp's previous tile
+    unsigned long long st_tiles = 0, st_chunks = 0, st_stages = 0, st_cuts = 0;
+    search::Counters cnt;
+    const int n_tiles = t.ctr[0];
+
+    for (;;) {
+        int ti = 0;
+        if (lane == 0) ti = atomicAdd(&t.ctr[1], 1);
+        ti = __shfl_sync(FG_FULL_MASK, ti, 0);
+        if (ti >= n_tiles) break;
+        ++st_tiles;
+        const int2 td = t.tiles[ti];
+        const int blk = td.x, start = td.y;
+        const int s = blk / t.bps;
+        int o[NL > 0 ? NL : 1];
+        tile::block_origin<NL>(blk - s * t.bps, t.nblk, o);
+        const int64_t cbase = (int64_t)s * t.total;
+
+        // ---- lane -> point (start + lane) of the block in (column, row) order
+        int col = 0;
+        if (lane < nb) {
+#pragma unroll
+            for (int rr = 0; rr < (1 << NL); ++rr) {
+                int rowflat = 0;
+                bool ok = true;
+#pragma unroll
+                for (int i = 0; i < NL; ++i) {
+                    const int j = o[i] + ((rr >> (NL - 1 - i)) & 1);
+                    ok &= j < nb;
+                    rowflat = rowflat * nb + j;
+                }
+                if (ok) {
+                    const int64_t rc = cbase + (int64_t)rowflat * nb + lane;
+                    col += t.bounds[rc + 1] - t.bounds[rc];
+                }
+            }
+        }
+        const int P = warp_inclusive_scan(col);
+        const int g = start + lane;
+        int c = 0;
+        for (int cc = 0; cc < nb; ++cc) c += __shfl_sync(FG_FULL_MASK, P, cc) <= g ? 1 : 0;
+        const int Ptot = __shfl_sync(FG_FULL_MASK, P, 31);
+        const int Pprev = __shfl_sync(FG_FULL_MASK, P, max(c - 1, 0));
+        int32_t p = -1;
+        if (g < Ptot && c < nb) {
+            int off = g - (c > 0 ? Pprev : 0);
+            for (int rr = 0; rr < (1 << NL); ++rr) {
+                int rowflat = 0;
+                bool ok = true;
+#pragma unroll
+                for (int i = 0; i < NL; ++i) {
+                    const int j = o[i] + ((rr >> (NL - 1 - i)) & 1);
+                    ok &= j < nb;
+                    rowflat = rowflat * nb + j;
+                }
+                if (!ok) continue;
+                const int64_t rc = cbase + (int64_t)rowflat * nb + c;
+                const int32_t b0 = t.bounds[rc], len = t.bounds[rc + 1] - b0;
+                if (off < len) {
+                    p = b0 + off;
+                    break;
+                }
+                off -= len;
+            }
+        }
+        const bool live = p >= 0;
+        if (!__any_sync(FG_FULL_MASK, live)) continue;
+        const int32_t qid = live ? a.sid[p] : 0;
+        // DirectionMask: roles 0/2 run no query (row = self + padding, pyx:210-211)
+        const bool active = live && need > 0 &&
+                            !(use_dir && (a.dir[qid] == 0 || a.dir[qid] == 2));
+
+        // ---- queries: coordinates (packed pairs), cell-unit box of the tile
+        float q[4 * NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            const float4 x = live ? t.sc[(int64_t)p * NV + v] : make_float4(0.f, 0.f, 0.f, 0.f);
+            q[4 * v] = x.x; q[4 * v + 1] = x.y; q[4 * v + 2] = x.z; q[4 * v + 3] = x.w;
+        }
+        unsigned long long qd[DE];
+#pragma unroll
+        for (int d = 0; d < DE; ++d) qd[d] = dup2(q[d]);
+        float w[DB], invw[DB], lo[DB], hi[DB];
+        float diag2 = 0.0f;  // squared diagonal of the split's grid box
+        float slack = kSlackCells;
+#pragma unroll
+        for (int i = 0; i < DB; ++i) {
+            const float mn = (float)t.mins[(int64_t)s * DB + i];
+            w[i] = (float)t.widths[(int64_t)s * DB + i];
+            invw[i] = __frcp_rn(w[i]);
+            const float qc = (q[i] - mn) * invw[i];
+            lo[i] = tile::warp_min_f(live ? qc : kInf);
+            hi[i] = tile::warp_max_f(live ? qc : -kInf);
+            diag2 = fmaf((float)nb * w[i], (float)nb * w[i], diag2);
+            if (X64) slack = fmaxf(slack, 2.0f * r * invw[i] + kSlackCells);
+        }
+        diag2 *= 1.01f;
+
+        // ---- staged region growth
+        float tt = kInf;  // true bound on the lane's keep-th smallest float64 d2
+        if (use_r2) tt = (float)(a.max_r2 * (1.0 + 2e-5)) + kTiny;
+        float tau = X64 ? up_bound(tt, r) : (use_r2 ? tt * kMargin : tt);
+        if (!active) {  // appends nothing, needs no region
+            tau = -1.0f;
+            tt = 0.0f;
+        }
+        int m = 0;
+        float rho2 = rho2_hint;
+        if (!(rho2 > 0.0f)) {  // no hint: a one-cell pilot
+            float wm = w[0];
+#pragma unroll
+            for (int i = 1; i < DB; ++i) wm = fminf(wm, w[i]);
+            rho2 = wm * wm;
+        }
+        rho2 = fminf(rho2, diag2);
+        Box<NL> prev = make_box<DB>(-1.0f, lo, hi, invw, nb, slack);
+        for (;;) {
+            ++st_stages;
+            const Box<NL> cur = make_box<DB>(rho2, lo, hi, invw, nb, slack);
+            for (int rb = 0; rb < cur.rows; rb += 32) {
+                const int rw = rb + lane;
+                int32_t S0 = 0, L0 = 0, S1 = 0, L1 = 0;
+                if (rw < cur.rows) {
+                    int jd[NL > 0 ? NL : 1];
+                    search::decode_row<NL>(rw, cur.L, cur.N, cur.inv, jd);
+                    int rowflat = 0;
+#pragma unroll
+                    for (int i = 0; i < NL; ++i) rowflat = rowflat * nb + jd[i];
+                    int ca, cb, pa, pb;
+                    row_piece<DB>(cur, jd, lo, hi, w, invw, nb, ca, cb);
+                    row_piece<DB>(prev, jd, lo, hi, w, invw, nb, pa, pb);
+                    const int64_t rc = cbase + (int64_t)rowflat * nb;
+                    if (ca <= cb) {
+                        if (pa > pb) {  // row new in this stage
+                            S0 = t.bounds[rc + ca];
+                            L0 = t.bounds[rc + cb + 1] - S0;
+                        } else {  // the shell: [ca, pa-1] and [pb+1, cb]
+                            if (ca < pa) {
+                                S0 = t.bounds[rc + ca];
+                                L0 = t.bounds[rc + pa] - S0;
+                            }
+                            if (pb < cb) {
+                                S1 = t.bounds[rc + pb + 1];
+                                L1 = t.bounds[rc + cb + 1] - S1;
+                            }
+                        }
+                    }
+                }
+                scan_spans<NV, DE, X64>(W, a, S0, L0, qd, tau, tt, m, keep, q, qid, r, bd_base,
+                                        bp_base, st_chunks, st_cuts);
+                scan_spans<NV, DE, X64>(W, a, S1, L1, qd, tau, tt, m, keep, q, qid, r, bd_base,
+                                        bp_base, st_chunks, st_cuts);
+            }
+            // tighten every lane to its keep-th smallest entry
+            unsigned todo = __ballot_sync(FG_FULL_MASK, active && m >= keep);
+            while (todo) {
+                const int j = __ffs(todo) - 1;
+                todo &= todo - 1;
+                const int mj = __shfl_sync(FG_FULL_MASK, m, j);
+                float qj[4 * NV];
+#pragma unroll
+                for (int d = 0; d < 4 * NV; ++d) qj[d] = __shfl_sync(FG_FULL_MASK, q[d], j);
+                const int32_t qidj = __shfl_sync(FG_FULL_MASK, qid, j);
+                const int rr = cut_lane<NV, X64, DE>(W, a, j, mj, keep, tau, tt, qj, qidj, r);
+                if (lane == j) m = rr;
+            }
+            const float need_t = tile::warp_max_f(active ? tt : 0.0f);
+            prev = cur;
+            // done when every lane's tt-ball is inside the region, or the region
+            // is the whole grid box of the split (lanes short of k-1 points)
+            if (need_t <= rho2 || rho2 >= diag2) break;
+            // grow: at most x1.6 in radius per stage, never past what is needed
+            rho2 = fminf(fminf(need_t, rho2 * 2.56f), diag2);
+        }
+        {
+            const float h = tile::warp_max_f(active ? tt : 0.0f);
+            rho2_hint = (h > 0.0f && h < kInf) ? h : -1.0f;
+        }
+
+        // ---- epilogue, one row at a time
+        const unsigned rows = __ballot_sync(FG_FULL_MASK, live);
+        for (unsigned mask = rows; mask;) {
+            const int j = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const int mj = __shfl_sync(FG_FULL_MASK, m, j);
+            const int32_t pj = __shfl_sync(FG_FULL_MASK, p, j);
+            const float tj = __shfl_sync(FG_FULL_MASK, tau, j);
+            const int32_t qj_id = __shfl_sync(FG_FULL_MASK, qid, j);
+            const bool aj = __shfl_sync(FG_FULL_MASK, active ? 1 : 0, j);
+            const int64_t row_out = (int64_t)qj_id * a.k;
+            if (lane == 0) {
+                a.out_idx[row_out] = qj_id;
+                search::store_d2(a, row_out, 0.0);
+            }
+            if (!aj) {  // no query: padding
+                for (int sl = 1 + lane; sl < a.k; sl += 32) {
+                    a.out_idx[row_out + sl] = -1;
+                    search::store_d2(a, row_out + sl, 0.0);
+                }
+                continue;
+            }
+            float qj[4 * NV];
+#pragma unroll
+            for (int d = 0; d < 4 * NV; ++d) qj[d] = __shfl_sync(FG_FULL_MASK, q[d], j);
+            // lane j's entries minus self
+            int wpos = 0;
+            for (int e0 = 0; e0 < mj; e0 += 32) {
+                const int e = e0 + lane;
+                const bool ok = e < mj && W.bp[j * kStride + e] != pj;
+                const unsigned bal = __ballot_sync(FG_FULL_MASK, ok);
+                if (ok) {
+                    const int at = wpos + __popc(bal & lanemask_lt());
+                    W.eb.d[at] = W.bd[j * kStride + e];
+                    W.eb.p[at] = W.bp[j * kStride + e];
+                }
+                wpos += __popc(bal);
+            }
+            __syncwarp();
+            if constexpr (X64) {
+                exact_sort<NV, X64, DE>(W, a, wpos, qj, qj_id);
+                for (int sl = 1 + lane; sl < a.k; sl += 32) {
+                    const int e = sl - 1;
+                    const unsigned long long kk = e < wpos ? W.eb.key[e] : ~0ull;
+                    if (kk != ~0ull) {
+                        a.out_idx[row_out + sl] = W.eb.id[e];
+                        search::store_d2(a, row_out + sl, __longlong_as_double((long long)kk));
+                    } else {
+                        a.out_idx[row_out + sl] = -1;
+                        search::store_d2(a, row_out + sl, 0.0);
+                    }
+                }
+                __syncwarp();
+            } else {
+                search::finish_query<NV, 128>(a, W.eb, qj, wpos, need, tj, row_out, cnt);
+            }
+        }
+        __syncwarp();
+    }
+    if (a.stats && lane == 0) {
+        unsigned long long* hs = a.stats + search::ST_COUNT + tile::TS_COUNT;
+        atomicAdd(&hs[HS_TILES], st_tiles);
+        atomicAdd(&hs[HS_CHUNKS], st_chunks);
+        atomicAdd(&hs[HS_STAGES], st_stages);
+        atomicAdd(&hs[HS_COMPACT], st_cuts);
+    }
+}
+
+// float64 mode: r = sqrt(n_c) x the largest difference error of two float32-
+// rounded coordinates (2 x 2^-24 x max |x|, plus the subnormal floor).
+static __global__ void k_abs_bound(const double* __restrict__ x, int64_t m, int n_c,
+                            unsigned* __restrict__ out) {
+    double mx = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x)
+        mx = fmax(mx, fabs(x[i]));
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FG_FULL_MASK, mx, o));
+    if (lane_id() == 0) {
+        const double e = 2.0 * (mx * 0x1p-24 + 0x1p-149);
+        const float rb = __double2float_ru(e * sqrt((double)n_c) * 1.0001);
+        atomicMax(out, __float_as_uint(rb));  // non-negative floats order like their bits
+    }
+}
+
+// Tile list, then the search (no redo: cuts fall back to exact keys).
+template <int NV, int DB, int DE, bool X64>
+int launch_hd(tile::TileArgs& t, const search::KnnArgs& a, cudaStream_t st) {
+    FG_CUDA(cudaMemsetAsync(t.ctr, 0, 8 * sizeof(int), st));
+    k_hd_tiles<DB><<<(unsigned)ceil_div(t.n_blocks, 4), 128, 0, st>>>(t);
+    FG_TRY(launched(st));
+    int dev = 0, sms = 0;
+    FG_CUDA(cudaGetDevice(&dev));
+    FG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    constexpr size_t smem = hd_smem_bytes<DE>();
+    auto kern = k_hd_search<NV, DB, DE, X64>;
+    FG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int per_sm = (int)std::max<size_t>(1, (227 * 1024) / (smem + 1024));
+    kern<<<(unsigned)(sms * per_sm), kWarps * 32, smem, st>>>(t, a);
+    return launched(st);
+}
+
+template <int NV, bool X64>
+int dispatch_db(tile::TileArgs& t, const search::KnnArgs& a, int d_bin, cudaStream_t st) {
+    switch (d_bin) {
+        case 1: return launch_hd<NV, 1, 4 * NV, X64>(t, a, st);
+        case 2: return launch_hd<NV, 2, 4 * NV, X64>(t, a, st);
+        case 3: return launch_hd<NV, 3, 4 * NV, X64>(t, a, st);
+        case 4: return launch_hd<NV, 4, 4 * NV, X64>(t, a, st);
+        default:
+            if constexpr (NV >= 2) {
+                if constexpr (NV == 3 && !X64) {  // d = 10 (config C): no padded dims in the hot loop
+                    if (a.n_c == 10) return launch_hd<NV, 5, 10, X64>(t, a, st);
+                }
+                return launch_hd<NV, 5, 4 * NV, X64>(t, a, st);
+            }
+            return FG_ERR_TOO_FEW_DIMS;
+    }
+}
+
+int dispatch_hd_nv1(tile::TileArgs& t, const search::KnnArgs& a, int d_bin, cudaStream_t st);
+int dispatch_hd_nv2(tile::TileArgs& t, const search::KnnArgs& a, int d_bin, cudaStream_t st);
+int dispatch_hd_nv3(tile::TileArgs& t, const search::KnnArgs& a, int d_bin, cudaStream_t st);
+int dispatch_hd_nv4(tile::TileArgs& t, const search::KnnArgs& a, int d_bin, cudaStream_t st);
+
+}  // namespace hd
+}  // namespace fg

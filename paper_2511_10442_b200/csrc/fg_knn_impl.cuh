@@ -97,6 +97,10 @@ struct KnnArgs {
     const int* qcount;          // tile path's redo list; its length lives on the device
     const int* qall;            // with qlist: *qall * 4 > n -> every query instead (the
                                 // tile kernels declined the data, fg_knn_tile.cuh)
+    const double* x64;          // float64 coordinates (original order, n x n_c) or null:
+                                // exact keys from them (fg_knn_hd.cuh float64 mode)
+    const float* rnd;           // float64 mode: device bound on |fp32 - float64| coordinate
+                                // differences x sqrt(n_c) (k_abs_bound)
 };
 
 template <int CAP>

@@ -32,8 +32,8 @@ constexpr int kThreads = 256;       // queries per block
 constexpr int kTileDoubles = 4096;  // staged candidate coordinates (32 KB)
 constexpr int kMaxK = 128;
 
-template <int NC>
-__global__ void __launch_bounds__(kThreads) k_brute(const float* __restrict__ coords, int n_c,
+template <int NC, typename TC>
+__global__ void __launch_bounds__(kThreads) k_brute(const TC* __restrict__ coords, int n_c,
                                                     const int64_t* __restrict__ rs, int n_splits,
                                                     const int32_t* __restrict__ queries, int64_t n_q,
                                                     const int8_t* __restrict__ dir, double max_r2,
@@ -125,10 +125,12 @@ __global__ void __launch_bounds__(kThreads) k_brute(const float* __restrict__ co
 
 }  // namespace
 
-extern "C" int fg_brute_knn(const float* coords, int64_t n, int32_t n_coords, const int64_t* row_splits,
-                            int32_t n_splits, const int32_t* queries, int64_t n_queries,
-                            const int8_t* dir_mask, double max_radius2, uint32_t flags, int32_t k,
-                            int32_t* out_idx, double* out_d2, void* stream) {
+namespace {
+template <typename TC>
+int brute_entry(const TC* coords, int64_t n, int32_t n_coords, const int64_t* row_splits,
+                int32_t n_splits, const int32_t* queries, int64_t n_queries, const int8_t* dir_mask,
+                double max_radius2, uint32_t flags, int32_t k, int32_t* out_idx, double* out_d2,
+                void* stream) {
     if (k < 1 || k > kMaxK) return FG_ERR_BAD_K;
     if (n < 0 || n >= ((int64_t)1 << 31) || n_splits < 1 || n_queries < 0) return FG_ERR_BAD_SHAPE;
     if (n_coords < 1) return FG_ERR_BAD_SHAPE;
@@ -143,12 +145,30 @@ extern "C" int fg_brute_knn(const float* coords, int64_t n, int32_t n_coords, co
     cudaStream_t st = (cudaStream_t)stream;
     const unsigned blocks = (unsigned)((nq + kThreads - 1) / kThreads);
     switch ((n_coords + 3) / 4) {
-        case 1: k_brute<4><<<blocks, kThreads, 0, st>>>(coords, n_coords, row_splits, n_splits, queries, nq, dir, max_radius2, use_r2, k, out_idx, out_d2); break;
-        case 2: k_brute<8><<<blocks, kThreads, 0, st>>>(coords, n_coords, row_splits, n_splits, queries, nq, dir, max_radius2, use_r2, k, out_idx, out_d2); break;
-        case 3: k_brute<12><<<blocks, kThreads, 0, st>>>(coords, n_coords, row_splits, n_splits, queries, nq, dir, max_radius2, use_r2, k, out_idx, out_d2); break;
-        default: k_brute<16><<<blocks, kThreads, 0, st>>>(coords, n_coords, row_splits, n_splits, queries, nq, dir, max_radius2, use_r2, k, out_idx, out_d2); break;
+        case 1: k_brute<4, TC><<<blocks, kThreads, 0, st>>>(coords, n_coords, row_splits, n_splits, queries, nq, dir, max_radius2, use_r2, k, out_idx, out_d2); break;
+        case 2: k_brute<8, TC><<<blocks, kThreads, 0, st>>>(coords, n_coords, row_splits, n_splits, queries, nq, dir, max_radius2, use_r2, k, out_idx, out_d2); break;
+        case 3: k_brute<12, TC><<<blocks, kThreads, 0, st>>>(coords, n_coords, row_splits, n_splits, queries, nq, dir, max_radius2, use_r2, k, out_idx, out_d2); break;
+        default: k_brute<16, TC><<<blocks, kThreads, 0, st>>>(coords, n_coords, row_splits, n_splits, queries, nq, dir, max_radius2, use_r2, k, out_idx, out_d2); break;
     }
     fg::g_launches.fetch_add(1, std::memory_order_relaxed);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 0 : (int)e;
+}
+}  // namespace
+
+extern "C" int fg_brute_knn(const float* coords, int64_t n, int32_t n_coords, const int64_t* row_splits,
+                            int32_t n_splits, const int32_t* queries, int64_t n_queries,
+                            const int8_t* dir_mask, double max_radius2, uint32_t flags, int32_t k,
+                            int32_t* out_idx, double* out_d2, void* stream) {
+    return brute_entry<float>(coords, n, n_coords, row_splits, n_splits, queries, n_queries,
+                              dir_mask, max_radius2, flags, k, out_idx, out_d2, stream);
+}
+
+extern "C" int fg_brute_knn_f64(const double* coords, int64_t n, int32_t n_coords,
+                                const int64_t* row_splits, int32_t n_splits, const int32_t* queries,
+                                int64_t n_queries, const int8_t* dir_mask, double max_radius2,
+                                uint32_t flags, int32_t k, int32_t* out_idx, double* out_d2,
+                                void* stream) {
+    return brute_entry<double>(coords, n, n_coords, row_splits, n_splits, queries, n_queries,
+                               dir_mask, max_radius2, flags, k, out_idx, out_d2, stream);
 }

@@ -113,7 +113,8 @@ def knn_backward(cloud: PointCloud, neighbors: NeighborMatrix, upstream) -> torc
         raise ShapeMismatchError(f"neighbours cover {neighbors.n_vertices} vertices, "
                                  f"cloud has {cloud.n_vertices}")
     n, k = neighbors.indices.shape
-    det = n <= (1 << 23) and n * k < (1 << 32)
+    det = (n <= (1 << 23) and n * k < (1 << 32) and cloud.coords.dtype == torch.float32
+           and up.dtype != torch.float64)
     return ops.binned_select_knn_grad(up, neighbors.indices, cloud.coords.detach(), None, det)
 
 

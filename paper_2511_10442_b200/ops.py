@@ -50,7 +50,7 @@ def set_debug_flags(flags: int) -> None:
 def knn_stats(reset: bool = True) -> dict:
     names = ("queries", "regions", "chunks", "appends", "compactions", "spec_fail", "exact_epi",
              "rows", "tiles", "tile_candidates", "tile_redo", "tile_fail", "tile_expanded",
-             "tile_evaluated")
+             "tile_evaluated", "hd_tiles", "hd_chunks", "hd_stages", "hd_redo", "hd_cuts")
     buf = (ctypes.c_uint64 * len(names))()
     _lib.check(_lib.load().fg_knn_stats(ctypes.cast(buf, ctypes.c_void_p), len(names), int(reset)))
     return dict(zip(names, [int(x) for x in buf]))
@@ -100,7 +100,10 @@ def bin_by_coordinates(coords: Tensor, row_splits: Tensor, d_bin: int,
     dev = coords.device
     if coords.dim() != 2:
         raise BadShapeError("coords must be 2-d (n_vertices, n_coords)")
-    coords = coords.to(torch.float32).contiguous()
+    # float64 coordinates (the reference's dtype) are binned from their float64
+    # values: every array bit-identical to the reference for any finite input
+    x64 = coords.dtype == torch.float64
+    coords = coords.contiguous() if x64 else coords.to(torch.float32).contiguous()
     rs = row_splits.to(device=dev, dtype=torch.int64).contiguous()
     n, n_c = coords.shape
     S = rs.numel() - 1
@@ -113,10 +116,10 @@ def bin_by_coordinates(coords: Tensor, row_splits: Tensor, d_bin: int,
     sorted_coords = torch.empty((n, coord_stride(n_c)), dtype=torch.float32, device=dev)
     nbytes = _lib.size_out(L.fg_bin_workspace_size, n, S, d_bin, n_bins)
     ws = _ws(nbytes, dev)
-    _lib.check(L.fg_bin_by_coordinates(_p(coords), n, n_c, _p(rs), S, d_bin, n_bins, _p(bin_idx),
-                                       _p(sort_order), _p(bounds), _p(mins), _p(widths),
-                                       _p(sorted_coords), _p(ws), ws.numel(), _stream(coords)),
-               "bin_by_coordinates")
+    fn = L.fg_bin_by_coordinates_f64 if x64 else L.fg_bin_by_coordinates
+    _lib.check(fn(_p(coords), n, n_c, _p(rs), S, d_bin, n_bins, _p(bin_idx), _p(sort_order),
+                  _p(bounds), _p(mins), _p(widths), _p(sorted_coords), _p(ws), ws.numel(),
+                  _stream(coords)), "bin_by_coordinates")
     return bin_idx, sort_order, bounds, mins, widths, sorted_coords
 
 
@@ -176,6 +179,18 @@ def binned_select_knn(coords: Tensor, row_splits: Tensor, bin_idx: Tensor, sort_
     flags |= _DEBUG_FLAGS
     idx = torch.empty((n, K), dtype=torch.int32, device=dev)
     d2 = torch.empty((n, K), dtype=torch.float64 if d2_f64 else torch.float32, device=dev)
+    if coords.dtype == torch.float64:
+        # exact float64 keys from the float64 coordinates (fg_knn_fwd_f64_ws)
+        x = coords.detach().to(dev).contiguous()
+        nbytes = _lib.size_out(L.fg_knn_f64_workspace_size, n, n_c, S, d_bin, n_bins, K, flags)
+        ws = _ws(nbytes, dev)
+        _lib.check(L.fg_knn_fwd_f64_ws(_p(x), _p(sorted_coords), _p(sort_order), _p(bin_idx),
+                                       _p(bin_bounds), _p(rs), _p(dim_mins), _p(widths), n, n_c,
+                                       S, d_bin, n_bins, K, _p(dir_t),
+                                       float(max_radius2 or 0.0), flags, _p(idx), _p(d2), _p(ws),
+                                       ws.numel(), _stream(sorted_coords)),
+                   "binned_select_knn (float64 coordinates)")
+        return idx, d2
     nbytes = _lib.size_out(L.fg_knn_workspace_size, n, n_c, S, d_bin, n_bins, K, flags)
     ws = _ws(nbytes, dev)
     _lib.check(L.fg_knn_fwd_ws(_p(sorted_coords), _p(sort_order), _p(bin_idx), _p(bin_bounds),
@@ -206,8 +221,12 @@ def binned_select_knn_grad(grad_d2: Tensor, idx: Tensor, coords: Tensor,
                                  f"{tuple(idx.shape)}")
     if idx.shape[0] != n:
         raise ShapeMismatchError(f"neighbours cover {idx.shape[0]} vertices, cloud has {n}")
-    c = coords.to(torch.float32).contiguous()
-    g = grad_d2.to(torch.float32).contiguous()
+    # float64 inputs keep their dtype (terms formed as numpy forms them); the
+    # deterministic kernel takes float32 inputs
+    x64 = coords.dtype == torch.float64 and not deterministic
+    g64 = grad_d2.dtype == torch.float64 and not deterministic
+    c = coords.contiguous() if x64 else coords.to(torch.float32).contiguous()
+    g = grad_d2.contiguous() if g64 else grad_d2.to(torch.float32).contiguous()
     ix = idx.to(torch.int32).contiguous()
     out_f64 = coords.dtype == torch.float64
     grad = torch.empty((n, n_c), dtype=torch.float64 if out_f64 else torch.float32,
@@ -215,6 +234,7 @@ def binned_select_knn_grad(grad_d2: Tensor, idx: Tensor, coords: Tensor,
     ws = _ws(_lib.size_out(L.fg_knn_bwd_workspace_size, n, n_c, k), coords.device)
     od = _order(order, n, coords.device)
     flags = (_lib.FG_BWD_F64 if out_f64 else 0) | (_lib.FG_BWD_DETERMINISTIC if deterministic else 0)
+    flags |= (_lib.FG_BWD_X64 if x64 else 0) | (_lib.FG_BWD_G64 if g64 else 0)
     _lib.check(L.fg_knn_bwd(_p(c), n, n_c, _p(ix), k, _p(g), _p(od), _p(grad), flags,
                             _p(ws), ws.numel(), _stream(c)), "binned_select_knn_grad")
     return grad
@@ -404,7 +424,8 @@ def brute_knn(coords: Tensor, row_splits: Tensor, K: int, queries: Optional[Tens
     L = _lib.load()
     dev = coords.device
     n, n_c = coords.shape
-    c = coords.to(torch.float32).contiguous()
+    x64 = coords.dtype == torch.float64
+    c = coords.contiguous() if x64 else coords.to(torch.float32).contiguous()
     rs = row_splits.to(device=dev, dtype=torch.int64).contiguous()
     q = None if queries is None else queries.to(device=dev, dtype=torch.int32).contiguous()
     nq = n if q is None else q.numel()
@@ -417,9 +438,9 @@ def brute_knn(coords: Tensor, row_splits: Tensor, K: int, queries: Optional[Tens
         flags |= _lib.FG_KNN_USE_MAX_R2
     idx = torch.empty((nq, K), dtype=torch.int32, device=dev)
     d2 = torch.empty((nq, K), dtype=torch.float64, device=dev)
-    _lib.check(L.fg_brute_knn(_p(c), n, n_c, _p(rs), rs.numel() - 1, _p(q), nq, _p(dr),
-                              float(max_radius2 or 0.0), flags, K, _p(idx), _p(d2), _stream(c)),
-               "brute_knn")
+    fn = L.fg_brute_knn_f64 if x64 else L.fg_brute_knn
+    _lib.check(fn(_p(c), n, n_c, _p(rs), rs.numel() - 1, _p(q), nq, _p(dr),
+                  float(max_radius2 or 0.0), flags, K, _p(idx), _p(d2), _stream(c)), "brute_knn")
     return idx, d2
 
 

@@ -66,9 +66,16 @@ def test_validation_before_launch():
                                None, 0.0, 0, None, None, None, ws_bytes, None)
     assert knn_ws(0, k=0) == -1
     assert knn_ws(0) == -5
-    # the tile path needs scratch; the warp-per-query path (here d_bin < n_c) needs none
+    # the tile paths need scratch (d <= 4 tiles; high-dimensional tiles for n_c > 4,
+    # k <= 64); the warp-per-query kernel (here k > 64) needs none
     assert L.fg_knn_workspace_size(1000, 4, 1, 4, 29, 40, 0, ctypes.byref(n)) == 0 and n.value > 4000
-    assert L.fg_knn_workspace_size(1000, 5, 1, 4, 29, 40, 0, ctypes.byref(n)) == 0 and n.value == 0
+    assert L.fg_knn_workspace_size(1000, 5, 1, 4, 29, 40, 0, ctypes.byref(n)) == 0 and n.value > 4000
+    assert L.fg_knn_workspace_size(1000, 5, 1, 4, 29, 80, 0, ctypes.byref(n)) == 0 and n.value == 0
+    assert L.fg_knn_f64_workspace_size(1000, 5, 1, 4, 29, 40, 0, ctypes.byref(n)) == 0 and n.value > 4000
+    def knn64(n=10, k=5):
+        return L.fg_knn_fwd_f64_ws(None, None, None, None, None, None, None, None, n, 4, 1, 4, 5, k,
+                                   None, 0.0, 0, None, None, None, 0, None)
+    assert knn64(k=0) == -1 and knn64() == -5
     assert L.fg_knn_workspace_size(1000, 4, 1, 4, 29, 40, _lib.FG_KNN_NO_TILE,
                                    ctypes.byref(n)) == 0 and n.value == 0
     # fused search + GravNet: float32 distances only, reducers validated before any launch
