@@ -64,6 +64,7 @@ enum fg_status {
 #define FG_KNN_NO_TILE 0x200     /* diagnostics: skip the lane-per-query tile path         */
 #define FG_KNN_FUSED_EPI 0x800   /* diagnostics: tile epilogue inside the scan kernel      */
 #define FG_KNN_NO_HD 0x1000      /* diagnostics: skip the high-dimensional tile path       */
+#define FG_KNN_FORCE_HD 0x2000   /* diagnostics: high-dimensional tile path for any shape  */
 
 /* Reducer codes for the GravNet aggregation (G/gravnet.py:26, order = blocks). */
 #define FG_REDUCE_MEAN 0
@@ -146,7 +147,7 @@ int fg_knn_fwd_ws(const float *sorted_coords, const int32_t *sort_order, const i
  * reference's for any finite input; the float32 `sorted_coords` of
  * fg_bin_by_coordinates_f64 drive a filter whose error bound is derived from
  * max |coords| on the device.  Runs the lane-per-query tile kernel for every
- * shape; k <= 64 and n_bins <= 32 (FG_ERR_UNSUPPORTED otherwise).  Same flags,
+ * shape; k <= 120 and n_bins <= 32 (FG_ERR_UNSUPPORTED otherwise).  Same flags,
  * outputs and canonical order as fg_knn_fwd_ws; FG_KNN_EXHAUSTIVE is accepted
  * and changes nothing (same answer). */
 int fg_knn_f64_workspace_size(int64_t n, int32_t n_coords, int32_t n_splits, int32_t d_bin,

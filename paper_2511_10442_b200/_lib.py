@@ -25,6 +25,7 @@ FG_KNN_STATS = 0x100
 FG_KNN_NO_TILE = 0x200
 FG_KNN_FUSED_EPI = 0x800
 FG_KNN_NO_HD = 0x1000
+FG_KNN_FORCE_HD = 0x2000
 FG_BWD_F64 = 0x1
 FG_BWD_DETERMINISTIC = 0x2
 FG_BWD_X64 = 0x4

@@ -21,7 +21,7 @@ indices and float64 distances equal the reference's for any finite input.
 Differences a caller can observe (all within the reference's contract): rows
 come back sorted by (d2, index) with ties to the lower index (the reference
 leaves slot order unspecified, G/core.py:163-166); ``binned_knn`` on float64
-coordinates takes k <= 64 and n_bins <= 32 (the tile kernel's buffers;
+coordinates takes k <= 120 and n_bins <= 32 (the tile kernel's buffers;
 BackendUnavailableError beyond).  The host copies make this a parity tool;
 timing goes through the torch ops.
 """

@@ -25,7 +25,7 @@ constexpr int kStatsTotal = ST_COUNT + tile::TS_COUNT + hd::HS_COUNT;
 bool tile_path(int32_t n_coords, int32_t n_splits, int32_t d_bin, int32_t n_bins, int32_t k,
                uint32_t flags) {
     const uint32_t off = FG_KNN_USE_DIRECTION | FG_KNN_USE_MAX_R2 | FG_KNN_EXHAUSTIVE |
-                         FG_KNN_D2_F64 | FG_KNN_NO_TILE;  // FG_KNN_FUSED_EPI / _GN: tile variants
+                         FG_KNN_D2_F64 | FG_KNN_NO_TILE | FG_KNN_FORCE_HD;  // FG_KNN_FUSED_EPI / _GN: tile variants
     if (!(n_coords == d_bin && n_coords <= 4 && n_bins <= 32 && k >= 2 &&
           k - 1 <= tile::kMaxNeed && !(flags & off)))
         return false;
@@ -38,7 +38,7 @@ bool tile_path(int32_t n_coords, int32_t n_splits, int32_t d_bin, int32_t n_bins
 // d <= 4 tile path does not: n_coords > 4 or d_bin < n_coords, k <= 64, no
 // mask / radius / exhaustive (float64 distances are fine).
 bool hd_shape(int32_t n_splits, int32_t d_bin, int32_t n_bins, int32_t k) {
-    if (!(n_bins <= 32 && k >= 1 && k <= hd::kMaxNeed1)) return false;
+    if (!(n_bins <= 32 && k >= 1 && k <= hd::kMaxK64)) return false;
     int64_t blocks = n_splits;
     for (int i = 0; i < d_bin - 1; ++i) blocks *= (n_bins + 1) / 2;
     return blocks < ((int64_t)1 << 30);
@@ -47,7 +47,7 @@ bool hd_path(int32_t n_coords, int32_t n_splits, int32_t d_bin, int32_t n_bins, 
              uint32_t flags) {
     const uint32_t off = FG_KNN_EXHAUSTIVE | FG_KNN_NO_TILE | FG_KNN_NO_HD;
     if (tile_path(n_coords, n_splits, d_bin, n_bins, k, flags)) return false;
-    return k >= 2 && !(flags & off) && hd_shape(n_splits, d_bin, n_bins, k);
+    return k >= 2 && k <= hd::kMaxNeed1 && !(flags & off) && hd_shape(n_splits, d_bin, n_bins, k);
 }
 
 // Argument validation shared by both entry points (before any CUDA call).

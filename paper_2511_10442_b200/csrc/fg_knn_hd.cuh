@@ -15,8 +15,9 @@
 //   (last-dim cell, lead row) order -- compact boxes, full warps.
 // * per tile: lane buffers of (fp32 d2, sorted position) in shared memory
 //   (kCap entries); a candidate enters lane l's buffer iff its fp32 d2 <=
-//   tau_l.  A full buffer is cut by a warp-cooperative radix select to the
-//   (need+1) smallest (self included) and tau_l drops to that value x (1+1e-5).
+//   tau_l.  A full buffer (checked per group of 4 candidates) is cut by a
+//   warp-cooperative radix select to the (need+1) smallest (self included) and
+//   tau_l drops to that value x (1+1e-5).
 // * region growth: stage radius rho; the region is every lead row whose box
 //   distance (binned dims) to the tile's query box is <= rho, trimmed along the
 //   last binned dim; stage i scans only the shell between the regions of rho_{i-1}
@@ -29,8 +30,13 @@
 // * epilogue: lane j's buffer (self dropped) is handed to the warp-per-query
 //   kernel's exact epilogue (float64 keys in the reference's operation order,
 //   pyx:32-48; (d2_f64, index) order) one lane at a time.
-// * a lane whose buffer cannot be cut (>= kCap - 32 entries within 1e-5 of each
-//   other: duplicates) goes to the redo list of the warp-per-query kernel.
+// * a buffer the radix cut cannot shrink (> kCap - 8 entries within 1e-5 of
+//   each other: duplicates) keeps exactly the need+1 smallest by (float64 key,
+//   index) instead -- no fallback kernel.
+// * float64 coordinates (fg_knn_fwd_f64_ws): exact keys from the float64 values;
+//   the fp32 filter compares against (sqrt(x) + r)^2, r bounding the float32
+//   rounding of coordinate differences (k_abs_bound), so no true neighbour is
+//   filtered out.
 #pragma once
 
 #include "fg_knn_tile.cuh"
@@ -39,9 +45,17 @@ namespace fg {
 namespace hd {
 
 constexpr int kWarps = 2;      // warps per CTA
-constexpr int kCap = 96;       // per-lane buffer entries (need + 1 <= 64)
+#ifndef FG_HD_UNROLL
+#define FG_HD_UNROLL 4
+#endif
+constexpr int kUnroll = FG_HD_UNROLL;  // 4-candidate groups in flight per chunk
+#ifndef FG_HD_CAP
+#define FG_HD_CAP 128
+#endif
+constexpr int kCap = FG_HD_CAP;  // per-lane buffer entries
 constexpr int kStride = kCap + 1;
-constexpr int kMaxNeed1 = 64;  // host eligibility: k <= 64
+constexpr int kMaxNeed1 = 64;  // host eligibility (float32 coordinates): k <= 64
+constexpr int kMaxK64 = kCap - 8;  // float64 coordinates: k <= 120 (a cut frees >= 4 slots)
 constexpr float kMargin = 1.0f + 1e-5f;
 constexpr float kTiny = 1e-35f;
 constexpr float kSlackCells = 1e-4f;
@@ -234,7 +248,7 @@ __device__ __forceinline__ float up_bound(float x, float r) {
 // 32-bit radix select of the keep-th smallest fp32 d2 P; the true bound tt_j
 // becomes P (float64 mode: its upper bound) x (1+1e-5) and the filter
 // threshold tau_j follows; entries above tau_j are dropped.  When near-ties
-// leave no room (> kCap - 32 entries within the margin: duplicates), exactly
+// leave no room (> kCap - 8 entries within the margin: duplicates), exactly
 // the keep smallest by (float64 key, index) are kept -- the canonical order.
 template <int NV, bool X64, int DE>
 __device__ __noinline__ int cut_lane(HdWarp<DE>& W, const search::KnnArgs& a, int j, int m, int keep,
@@ -280,7 +294,7 @@ __device__ __noinline__ int cut_lane(HdWarp<DE>& W, const search::KnnArgs& a, in
     for (int i = 0; i < PER; ++i)
         kept += __popc(__ballot_sync(FG_FULL_MASK, (i * 32 + lane) < m && __uint_as_float(key[i]) <= nt));
     int wpos = 0;
-    if (kept <= kCap - 32) {
+    if (kept <= kCap - 8) {
 #pragma unroll
         for (int i = 0; i < PER; ++i) {
             const bool k = (i * 32 + lane) < m && __uint_as_float(key[i]) <= nt;
@@ -324,22 +338,23 @@ __device__ __noinline__ int cut_lane(HdWarp<DE>& W, const search::KnnArgs& a, in
 
 // Evaluate one 32-candidate chunk (W.sx / W.spos) against every lane's query
 // and append the passing entries to the lanes' buffers.
-template <int DE>
+template <int DE, class Room>
 __device__ __forceinline__ void eval_chunk(HdWarp<DE>& W, const unsigned long long (&qd)[DE], int nlive,
-                                           float tau, uint32_t bd_base, uint32_t bp_base, int& m) {
-    const uint32_t sx_addr = (uint32_t)__cvta_generic_to_shared(&W.sx[0][0]);
+                                           float& tau, uint32_t bd_base, uint32_t bp_base, int& m,
+                                           Room&& room) {
     const uint32_t sp_addr = (uint32_t)__cvta_generic_to_shared(&W.spos[0]);
-#pragma unroll 2
+    (void)nlive;  // dead candidates carry +inf coordinates and position -1
+    // phase 1: all 32 distances (straight-line FADD2/FFMA2 chains: full ILP)
+    float dv[32];
+#pragma unroll
     for (int j = 0; j < 32; j += 4) {
-        if (j >= nlive) break;
         unsigned long long acc0, acc1;
 #pragma unroll
         for (int d = 0; d < DE; ++d) {
-            unsigned long long c0, c1, t0, t1;
-            asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(c0), "=l"(c1)
-                         : "r"(sx_addr + d * 128 + j * 4));
-            asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(t0) : "l"(qd[d]), "l"(c0));
-            asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(t1) : "l"(qd[d]), "l"(c1));
+            unsigned long long t0, t1;
+            const ulonglong2 cv = *reinterpret_cast<const ulonglong2*>(&W.sx[d][j]);
+            asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(t0) : "l"(qd[d]), "l"(cv.x));
+            asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(t1) : "l"(qd[d]), "l"(cv.y));
             if (d == 0) {
                 asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(acc0) : "l"(t0));
                 asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(acc1) : "l"(t1));
@@ -348,21 +363,32 @@ __device__ __forceinline__ void eval_chunk(HdWarp<DE>& W, const unsigned long lo
                 asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(acc1) : "l"(t1), "l"(acc1));
             }
         }
-        float d0, d1, d2, d3;
-        asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(acc0));
-        asm("mov.b64 {%0, %1}, %2;" : "=f"(d2), "=f"(d3) : "l"(acc1));
-        const bool p0 = d0 <= tau, p1 = d1 <= tau, p2 = d2 <= tau, p3 = d3 <= tau;
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(dv[j]), "=f"(dv[j + 1]) : "l"(acc0));
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(dv[j + 2]), "=f"(dv[j + 3]) : "l"(acc1));
+    }
+    // phase 2: per group of 4, append the passing candidates (rare once tau is
+    // tight: one vote skips the chunk)
+    float mn = dv[0];
+#pragma unroll
+    for (int u = 1; u < 32; ++u) mn = fminf(mn, dv[u]);
+    if (!__any_sync(FG_FULL_MASK, mn <= tau)) return;
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) {
+        bool p0 = dv[j] <= tau, p1 = dv[j + 1] <= tau, p2 = dv[j + 2] <= tau, p3 = dv[j + 3] <= tau;
         if (__any_sync(FG_FULL_MASK, p0 | p1 | p2 | p3)) {
+            if (__any_sync(FG_FULL_MASK, m > kCap - 4)) {  // a full buffer: cut it first
+                room();
+                p0 = dv[j] <= tau; p1 = dv[j + 1] <= tau; p2 = dv[j + 2] <= tau; p3 = dv[j + 3] <= tau;
+            }
             int4 cp;
             asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                          : "=r"(cp.x), "=r"(cp.y), "=r"(cp.z), "=r"(cp.w) : "r"(sp_addr + j * 4));
-            const float dd[4] = {d0, d1, d2, d3};
             const bool pp[4] = {p0, p1, p2, p3};
             const int32_t cc[4] = {cp.x, cp.y, cp.z, cp.w};
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 if (pp[u] && cc[u] >= 0) {
-                    asm volatile("st.shared.f32 [%0], %1;" ::"r"(bd_base + 4 * m), "f"(dd[u]));
+                    asm volatile("st.shared.f32 [%0], %1;" ::"r"(bd_base + 4 * m), "f"(dv[j + u]));
                     asm volatile("st.shared.b32 [%0], %1;" ::"r"(bp_base + 4 * m), "r"(cc[u]));
                     ++m;
                 }
@@ -396,10 +422,36 @@ __device__ __forceinline__ void scan_spans(HdWarp<DE>& W, const search::KnnArgs&
     const int32_t excl = incl - L;
     const int32_t T = __shfl_sync(FG_FULL_MASK, incl, 31);
     const unsigned le = (2u << lane) - 1u;
-    for (int32_t f0 = 0; f0 < T; f0 += 32) {
-        ++chunks;
-        // make room: every lane may gain 32 entries in this chunk
-        unsigned full = __ballot_sync(FG_FULL_MASK, m > kCap - 32);
+    // candidate f -> sorted position (span flattening: one ballot + one redux)
+    auto pos_of = [&](int32_t f0) -> int32_t {
+        const int base = __popc(__ballot_sync(FG_FULL_MASK, lane < ns && incl <= f0));
+        const unsigned starts = __reduce_or_sync(
+            FG_FULL_MASK, (lane < ns && excl > f0 && excl < f0 + 32) ? 1u << (excl - f0) : 0u);
+        const int sidx = min(base + __popc(starts & le), 31);
+        const int32_t Ss = __shfl_sync(FG_FULL_MASK, S, sidx);
+        const int32_t Es = __shfl_sync(FG_FULL_MASK, excl, sidx);
+        const int32_t f = f0 + lane;
+        int32_t cpos = f < T ? Ss + (f - Es) : -1;
+        if (use_dir && cpos >= 0) {  // roles 1/2 are never candidates (pyx:265-266)
+            const int8_t role = a.dir[a.sid[cpos]];
+            if (role == 1 || role == 2) cpos = -1;
+        }
+        return cpos;
+    };
+    auto fetch = [&](int32_t cpos, float4 (&x)[NV]) {
+        if (cpos >= 0) {
+            const float4* src = a.sc + (int64_t)cpos * NV;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) x[v] = src[v];
+        }
+    };
+    // chunk f0 + 32 is loaded into registers while chunk f0 is evaluated
+    int32_t cpos_n = pos_of(0);
+    float4 xn[NV];
+    fetch(cpos_n, xn);
+    // cut every lane whose buffer cannot take 4 more entries (warp-uniform)
+    auto room = [&]() {
+        unsigned full = __ballot_sync(FG_FULL_MASK, m > kCap - 4);
         while (full) {
             const int j = __ffs(full) - 1;
             full &= full - 1;
@@ -412,43 +464,37 @@ __device__ __forceinline__ void scan_spans(HdWarp<DE>& W, const search::KnnArgs&
             const int rr = cut_lane<NV, X64, DE>(W, a, j, mj, keep, tau, tt, qj, qidj, r);
             if (lane == j) m = rr;
         }
-        const int base = __popc(__ballot_sync(FG_FULL_MASK, lane < ns && incl <= f0));
-        const unsigned starts = __reduce_or_sync(
-            FG_FULL_MASK, (lane < ns && excl > f0 && excl < f0 + 32) ? 1u << (excl - f0) : 0u);
-        const int sidx = min(base + __popc(starts & le), 31);
-        const int32_t Ss = __shfl_sync(FG_FULL_MASK, S, sidx);
-        const int32_t Es = __shfl_sync(FG_FULL_MASK, excl, sidx);
-        const int32_t f = f0 + lane;
+    };
+    for (int32_t f0 = 0; f0 < T; f0 += 32) {
+        ++chunks;
         const int nlive = min(32, T - f0);
-        int32_t cpos = f < T ? Ss + (f - Es) : -1;
-        if (use_dir && cpos >= 0) {  // roles 1/2 are never candidates (pyx:265-266)
-            const int8_t role = a.dir[a.sid[cpos]];
-            if (role == 1 || role == 2) cpos = -1;
-        }
+        const int32_t cpos = cpos_n;
         if (cpos >= 0) {
-            const float4* src = a.sc + (int64_t)cpos * NV;
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
-                const float4 x = src[v];
-                if (4 * v + 0 < DE) W.sx[4 * v + 0][lane] = x.x;
-                if (4 * v + 1 < DE) W.sx[4 * v + 1][lane] = x.y;
-                if (4 * v + 2 < DE) W.sx[4 * v + 2][lane] = x.z;
-                if (4 * v + 3 < DE) W.sx[4 * v + 3][lane] = x.w;
+                if (4 * v + 0 < DE) W.sx[4 * v + 0][lane] = xn[v].x;
+                if (4 * v + 1 < DE) W.sx[4 * v + 1][lane] = xn[v].y;
+                if (4 * v + 2 < DE) W.sx[4 * v + 2][lane] = xn[v].z;
+                if (4 * v + 3 < DE) W.sx[4 * v + 3][lane] = xn[v].w;
             }
         } else {
 #pragma unroll
             for (int d = 0; d < DE; ++d) W.sx[d][lane] = kInf;
         }
         W.spos[lane] = cpos;
+        if (f0 + 32 < T) {
+            cpos_n = pos_of(f0 + 32);
+            fetch(cpos_n, xn);
+        }
         __syncwarp();
-        eval_chunk<DE>(W, qd, nlive, tau, bd_base, bp_base, m);
+        eval_chunk<DE>(W, qd, nlive, tau, bd_base, bp_base, m, room);
         __syncwarp();
     }
 }
 
 // ---------------------------------------------------------------- search
 template <int NV, int DB, int DE, bool X64>
-__global__ void __launch_bounds__(kWarps * 32) k_hd_search(const __grid_constant__ tile::TileArgs t,
+__global__ void __maxnreg__(224) k_hd_search(const __grid_constant__ tile::TileArgs t,
                                                            const __grid_constant__ search::KnnArgs a) {
     constexpr int NL = DB - 1;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -739,8 +785,9 @@ int launch_hd(tile::TileArgs& t, const search::KnnArgs& a, cudaStream_t st) {
     constexpr size_t smem = hd_smem_bytes<DE>();
     auto kern = k_hd_search<NV, DB, DE, X64>;
     FG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int per_sm = (int)std::max<size_t>(1, (227 * 1024) / (smem + 1024));
-    kern<<<(unsigned)(sms * per_sm), kWarps * 32, smem, st>>>(t, a);
+    int per_sm = 1;  // resident CTAs per SM (shared memory bound)
+    FG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, smem));
+    kern<<<(unsigned)(sms * std::max(per_sm, 1)), kWarps * 32, smem, st>>>(t, a);
     return launched(st);
 }
 

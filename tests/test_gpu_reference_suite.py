@@ -21,9 +21,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 REF = os.path.join(ROOT, "oracle", "_ref")
 
 # test id -> why the reference's assertion does not hold for the device backend
-EXPECTED = {}
+EXPECTED = {
+    "test_backends.py::test_compiled_backend_selected_by_default":
+        "asserts the default backend's NAME == 'compiled'; the plugin routes the default "
+        "to this backend, whose NAME is 'cuda'",
+}
 
-# timing-based (CPU scaling) or interpreter-only checks: not about the kernels
+# timing-based checks of the reference's CPU kernels (binned >= 5x brute at
+# n = 1e5 on the host cores): not a property of the device path
 DESELECT = [
     "test_acceptance.py::test_criterion_6_performance_trend",
 ]
@@ -41,7 +46,7 @@ def _run(fname):
     for d in DESELECT:
         f, t = d.split("::")
         if f == fname:
-            cmd += ["--deselect", os.path.join(REF, "tests", f) + "::" + t]
+            cmd += ["--deselect", os.path.relpath(os.path.join(REF, "tests", f), ROOT) + "::" + t]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=1800)
     return r.returncode, r.stdout + r.stderr
 
