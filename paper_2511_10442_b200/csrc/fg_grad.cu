@@ -221,8 +221,149 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) k_knn_bwd_pipe(
     }
 }
 
+// d == 4 (16-byte aligned float32 coordinates), k <= 65: a persistent warp
+// walks its rows (i, i + W, ... in `order`) as a software pipeline -- the
+// idx / upstream loads of row i+2 and the coordinate gathers of row i+1 are in
+// flight while row i's terms are formed and its returning hi atomics issue,
+// and the TwoSum corrections (lo REDs) of row i-1 go out once their atomics
+// have returned.  The query side of a row (a warp sum, exactly one writer) is
+// stored, not accumulated: qside[v].  Same arithmetic as k_knn_bwd_pipe.
+constexpr int kBwdChunk = 64;  // rows per CTA chunk (k_knn_bwd_stream)
+
+struct BwdRow {
+    int64_t v;
+    int32_t u[2];
+    float g[2];
+};
+
+__device__ __forceinline__ void bwd_load_row(BwdRow& r, int64_t i, int64_t n, const int32_t* __restrict__ order,
+                                             const int32_t* __restrict__ idx, const float* __restrict__ gd2,
+                                             int k) {
+    const int lane = lane_id();
+    r.v = i < n ? (order ? (int64_t)order[i] : i) : -1;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const int s = 1 + lane + 32 * q;
+        const bool ok = r.v >= 0 && s < k;
+        r.u[q] = ok ? __ldcs(idx + r.v * k + s) : -1;  // streamed once: evict first
+        r.g[q] = ok ? __ldcs(gd2 + r.v * k + s) : 0.0f;
+    }
+}
+
+__global__ void __launch_bounds__(kRowWarps * 32) k_knn_bwd_stream(
+    const float4* __restrict__ c4, int64_t n, const int32_t* __restrict__ idx, int k,
+    const float* __restrict__ gd2, const int32_t* __restrict__ order, float4* __restrict__ hi,
+    float4* __restrict__ lo, double4* __restrict__ qside) {
+    const int lane = lane_id();
+    // rows in chunks of kBwdChunk consecutive positions of the visiting order,
+    // dealt round-robin to the CTAs: a CTA's warps work on spatial neighbours
+    // (their neighbour gathers hit L1) and the rows in flight GPU-wide stay in
+    // one window of the order (the atomics' targets stay L2-resident)
+    constexpr int kPer = kBwdChunk / kRowWarps;  // rows per warp per chunk
+    const int j = threadIdx.x >> 5;
+    const int64_t G = gridDim.x;
+    auto row_of = [&](int64_t t) -> int64_t {
+        return ((int64_t)blockIdx.x + G * (t / kPer)) * kBwdChunk + j + kRowWarps * (t % kPer);
+    };
+    BwdRow r0, r1, r2;
+    float4 xv0, xu0[2], xv1, xu1[2];
+    auto gather = [&](const BwdRow& r, float4& xv, float4 (&xu)[2]) {
+        xv = r.v >= 0 ? c4[r.v] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) xu[q] = r.u[q] >= 0 ? c4[r.u[q]] : xv;
+    };
+    bwd_load_row(r0, row_of(0), n, order, idx, gd2, k);
+    bwd_load_row(r1, row_of(1), n, order, idx, gd2, k);
+    gather(r0, xv0, xu0);
+    // the previous row's pending corrections
+    int32_t pu[2] = {-1, -1};
+    float4 ph[2], pold[2];
+    double px[2][4];
+    for (int64_t t = 0; row_of(t) < n; ++t) {
+        bwd_load_row(r2, row_of(t + 2), n, order, idx, gd2, k);
+        gather(r1, xv1, xu1);
+        // row i: exact float64 terms, returning hi atomics
+        float4 h[2], old[2];
+        double x[2][4];
+        double qs[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const double tg = 2.0 * (double)r0.g[q];
+            const float4 a = xv0, b = xu0[q];
+            x[q][0] = tg * ((double)a.x - (double)b.x);
+            x[q][1] = tg * ((double)a.y - (double)b.y);
+            x[q][2] = tg * ((double)a.z - (double)b.z);
+            x[q][3] = tg * ((double)a.w - (double)b.w);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                qs[e] += x[q][e];
+                x[q][e] = -x[q][e];
+            }
+            h[q] = make_float4((float)x[q][0], (float)x[q][1], (float)x[q][2], (float)x[q][3]);
+            if (r0.u[q] >= 0) old[q] = atomicAdd(hi + r0.u[q], h[q]);
+        }
+        // row i-1: corrections (their atomics have returned by now)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            if (pu[q] < 0) continue;
+            const float* hp = &ph[q].x;
+            const float* op = &pold[q].x;
+            float4 l;
+            float* lp = &l.x;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                lp[e] = (float)(px[q][e] - (double)hp[e]);
+                const float a2 = op[e], b2 = hp[e];
+                const float sum = __fadd_rn(a2, b2);
+                const float bb = __fsub_rn(sum, a2);
+                const float err = __fadd_rn(__fsub_rn(a2, __fsub_rn(sum, bb)), __fsub_rn(b2, bb));
+                lp[e] = isfinite(sum) ? __fadd_rn(lp[e], err) : 0.f;
+            }
+            atomicAdd(lo + pu[q], l);
+        }
+        // row i: the query side, stored by its one writer
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) qs[e] += __shfl_xor_sync(FG_FULL_MASK, qs[e], o);
+        if (lane == 0 && r0.v >= 0) qside[r0.v] = make_double4(qs[0], qs[1], qs[2], qs[3]);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            pu[q] = r0.u[q];
+            ph[q] = h[q];
+            pold[q] = old[q];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) px[q][e] = x[q][e];
+        }
+        r0 = r1;
+        xv0 = xv1;
+        xu0[0] = xu1[0];
+        xu0[1] = xu1[1];
+        r1 = r2;
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {  // the last row's corrections
+        if (pu[q] < 0) continue;
+        const float* hp = &ph[q].x;
+        const float* op = &pold[q].x;
+        float4 l;
+        float* lp = &l.x;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            lp[e] = (float)(px[q][e] - (double)hp[e]);
+            const float a2 = op[e], b2 = hp[e];
+            const float sum = __fadd_rn(a2, b2);
+            const float bb = __fsub_rn(sum, a2);
+            const float err = __fadd_rn(__fsub_rn(a2, __fsub_rn(sum, bb)), __fsub_rn(b2, bb));
+            lp[e] = isfinite(sum) ? __fadd_rn(lp[e], err) : 0.f;
+        }
+        atomicAdd(lo + pu[q], l);
+    }
+}
+
 __global__ void k_bwd_finish(const float4* __restrict__ hi, const float4* __restrict__ lo, int64_t n,
-                             int n_c, int nv, void* __restrict__ out, int is_f64) {
+                             int n_c, int nv, void* __restrict__ out, int is_f64,
+                             const double* __restrict__ qside) {
     const int64_t m = n * n_c;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m;
          t += (int64_t)gridDim.x * blockDim.x) {
@@ -230,7 +371,8 @@ __global__ void k_bwd_finish(const float4* __restrict__ hi, const float4* __rest
         const int i = (int)(t - v * n_c);
         const float h = (&hi[v * nv + (i >> 2)].x)[i & 3];
         const float l = (&lo[v * nv + (i >> 2)].x)[i & 3];
-        const double x = (double)h + (double)l;
+        double x = (double)h + (double)l;
+        if (qside) x += qside[v * 4 + i];
         if (is_f64)
             reinterpret_cast<double*>(out)[t] = x;
         else
@@ -763,7 +905,9 @@ using namespace fg::grad;
 namespace {
 size_t fallback_bytes(int64_t n, int n_coords) {
     const int nv = (n_coords + 3) / 4;
-    return 2 * align_up(sizeof(float4) * (size_t)n * nv, 256);
+    // hi, lo (float4 per 4 coordinates) + the streamed kernel's query sides (d == 4)
+    return 2 * align_up(sizeof(float4) * (size_t)n * nv, 256) +
+           (n_coords == 4 ? align_up(sizeof(double) * 4 * (size_t)n, 256) : 0);
 }
 }  // namespace
 
@@ -806,13 +950,27 @@ extern "C" int fg_knn_bwd(const void* coords_v, int64_t n, int32_t n_coords, con
     }
     // compensated fp32x4 atomics
     const size_t half = align_up(sizeof(float4) * (size_t)n * nv, 256);
-    if (workspace_bytes < 2 * half) return FG_ERR_WORKSPACE;
+    if (workspace_bytes < fallback_bytes(n, n_coords)) return FG_ERR_WORKSPACE;
     float4* hi = (float4*)workspace;
     float4* lo = (float4*)((char*)workspace + half);
+    double* qside = nullptr;
     FG_CUDA(cudaMemsetAsync(workspace, 0, 2 * half, st));
     const unsigned blocks = (unsigned)ceil_div(n, kRowWarps);
     const bool vec4 = n_coords == 4 && (reinterpret_cast<uintptr_t>(coords) & 15) == 0;
-    if (x64 || g64) {
+#ifndef FG_BWD_STREAM
+#define FG_BWD_STREAM 1
+#endif
+    if (FG_BWD_STREAM && !x64 && !g64 && vec4 && k <= 65) {
+        qside = (double*)((char*)workspace + 2 * half);
+        int dev = 0, sms = 0, per_sm = 1;
+        FG_CUDA(cudaGetDevice(&dev));
+        FG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        FG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_knn_bwd_stream, kRowWarps * 32, 0));
+        const int64_t grid = std::min<int64_t>((int64_t)sms * std::max(per_sm, 1), blocks);
+        k_knn_bwd_stream<<<(unsigned)grid, kRowWarps * 32, 0, st>>>(
+            reinterpret_cast<const float4*>(coords), n, idx, k, grad_d2, order, hi, lo,
+            reinterpret_cast<double4*>(qside));
+    } else if (x64 || g64) {
         const double* c64 = static_cast<const double*>(coords_v);
         const double* g64p = static_cast<const double*>(grad_v);
 #define FG_BWD_GEN(NVV)                                                                              \
@@ -842,6 +1000,6 @@ extern "C" int fg_knn_bwd(const void* coords_v, int64_t n, int32_t n_coords, con
     FG_TRY(launched(st));
     const int64_t m = n * n_coords;
     k_bwd_finish<<<(unsigned)std::min<int64_t>(ceil_div(m, 256), 148 * 16), 256, 0, st>>>(
-        hi, lo, n, n_coords, nv, grad_coords, grad_is_f64);
+        hi, lo, n, n_coords, nv, grad_coords, grad_is_f64, qside);
     return launched(st);
 }
