@@ -244,8 +244,8 @@ __device__ __forceinline__ float up_bound(float x, float r) {
     return s * s * kMargin + kTiny;
 }
 
-// Warp-cooperative cut of lane j's buffer to its keep smallest entries: exact
-// 32-bit radix select of the keep-th smallest fp32 d2 P; the true bound tt_j
+// Warp-cooperative cut of lane j's buffer to its keep smallest entries: radix
+// select of (an upper bound within 2^-7 of) the keep-th smallest fp32 d2 P; the true bound tt_j
 // becomes P (float64 mode: its upper bound) x (1+1e-5) and the filter
 // threshold tau_j follows; entries above tau_j are dropped.  When near-ties
 // leave no room (> kCap - 8 entries within the margin: duplicates), exactly
@@ -271,8 +271,11 @@ __device__ __noinline__ int cut_lane(HdWarp<DE>& W, const search::KnnArgs& a, in
             hi_k = max(hi_k, key[i]);
         }
     }
-    lo_k = __reduce_min_sync(FG_FULL_MASK, lo_k);
-    hi_k = __reduce_max_sync(FG_FULL_MASK, hi_k);
+    // radix select on the top 16 bits (sign, exponent, 7 mantissa bits): P =
+    // an upper bound of the keep-th smallest fp32 d2 within 2^-7 of it (the
+    // entries sharing its 16-bit prefix stay; at most 16 rounds per cut)
+    lo_k = __reduce_min_sync(FG_FULL_MASK, lo_k) >> 16;
+    hi_k = __reduce_max_sync(FG_FULL_MASK, hi_k) >> 16;
     const int nbits = 32 - __clz(lo_k ^ hi_k);
     unsigned P = nbits >= 32 ? 0u : (lo_k & ~((1u << nbits) - 1u));
 #pragma unroll 1
@@ -280,12 +283,11 @@ __device__ __noinline__ int cut_lane(HdWarp<DE>& W, const search::KnnArgs& a, in
         const unsigned t = P | ((1u << bit) - 1u);
         int c = 0;
 #pragma unroll
-        for (int i = 0; i < PER; ++i) c += key[i] <= t ? 1 : 0;
+        for (int i = 0; i < PER; ++i) c += (key[i] >> 16) <= t ? 1 : 0;
         c = __reduce_add_sync(FG_FULL_MASK, c);
         if (c < keep) P |= 1u << bit;
     }
-    // P = the keep-th smallest fp32 d2 exactly
-    const float Pf = __uint_as_float(P);
+    const float Pf = __uint_as_float((P << 16) | 0xffffu);
     float tt = fminf(__shfl_sync(FG_FULL_MASK, tt_j, j), X64 ? up_bound(Pf, r) : Pf * kMargin + kTiny);
     float nt = X64 ? up_bound(tt, r) : tt;
     __syncwarp();
