@@ -51,7 +51,8 @@ C_TOTAL = {"A": 8.6e5, "B": 3.68e9, "north_star": 7.47e8, "C": 1.81e11, "D": 4.5
 # vertex stays a candidate, so the per-query cost is the full problem's)
 REF_QUERY_FRAC = {"north_star": 1.0, "A": 1.0, "B": 1.0, "C": 0.002, "D": 0.1, "E": 1.0}
 
-SEARCH_KERNELS = ("k_tiles", "k_tile_search", "k_tile_finish", "k_knn_fwd")
+SEARCH_KERNELS = ("k_tiles", "k_tile_search", "k_tile_finish", "k_knn_fwd", "k_hd_tiles",
+                  "k_hd_search")
 
 DESC = {"north_star": "north_star: 1 event x 1,000,000 uniform points per GPU, d=4, k=40",
         "A": "A: 10k points d=3 k=16", "B": "B: 200k clustered points d=4 k=40",
@@ -73,6 +74,17 @@ def load_peak():
             return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_fp32_peak():
+    """Measured FP32 CUDA-core peak (tools/micro/fp32_peak.cu, FFMA2) on this pool."""
+    path = os.path.join(ROOT, "profiles", "r2", "fp32_peak.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["ffma2_tflops"]), "measured (profiles/r2/fp32_peak.json, FFMA2 loop)"
+    except Exception:
+        return 74.4, "fallback (148 SMs x 128 FMA/clk x 2 x 1.965 GHz)"
 
 
 def load_traffic(config):
@@ -612,7 +624,26 @@ def main():
         compulsory += 4 * n * 64 + 4 * n * 128
     achieved = b_phase / (t_knn_ms * 1e-3) / 1e9
     traffic = load_traffic(args.config)
-    roof = {"bound": "hbm",
+    if d > 4:  # config C: the search is FP32 compute, not bytes (3 d C_total flops)
+        fpk, fpk_src = load_fp32_peak()
+        flops = 3.0 * d * c_total
+        ach = flops / (t_knn_ms * 1e-3) / 1e12
+        roof = {"bound": "fp32", "kernel": "binned_select_knn (k_hd_tiles + k_hd_search: lane-per-"
+                                          "query tiles, FADD2/FFMA2 over broadcast candidates)",
+                "achieved": ach, "peak": fpk, "unit": "TFLOP/s", "frac": ach / fpk,
+                "frac_kind": "model: SURVEY 8(d) 3*d*C_total fp32 flops (the reference algorithm's "
+                             "candidate count) / measured search time",
+                "flops_model": f"3 * d * C_total = 3 * {d} * {c_total:.3g}",
+                "peak_source": fpk_src, "traffic": traffic,
+                "compulsory_bytes": compulsory,
+                "binding": "SM issue / latency (ncu: IPC ~1.1-1.5 at 6 warps/SM, the per-lane "
+                           "buffers' shared memory bounds occupancy; profiles/r2/)",
+                "hbm_model_frac": achieved / peak}
+        b_phase = None
+    else:
+        roof = None
+    if roof is None:
+      roof = {"bound": "hbm",
             "kernel": ("knn_gravnet (k_tiles + k_tile_search + k_tile_finish + redo, then the "
                        "aggregation)") if gravnet else
                       "binned_select_knn (k_tiles + k_tile_search + k_tile_finish + k_knn_fwd redo)",
@@ -633,6 +664,8 @@ def main():
                        "SM throughput ~70%, DRAM < 15%; profiles/)",
             "peak_source": peak_src,
             "step_frac_model": (b_fwd + b_bwd) / (ms * 1e-3) / 1e9 / peak}
+      if d > 4 or d_bin < d:
+          roof["kernel"] = "binned_select_knn (k_hd_tiles + k_hd_search)"
     line = {
         "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -641,7 +674,8 @@ def main():
         "config": {**config_keys(args.config, n, d, k, n_bins,
                                  world if scaling == "weak" else 64, not args.no_flush),
                    "precision": "fp32 distance filter, float64 exact epilogue / gradient terms",
-                   "backward": "deterministic transposed" if det else "compensated fp32x4 atomics"},
+                   "backward": "deterministic transposed" if det else
+                               "compensated fp32x4 atomics (pipelined stream kernel for d = 4)"},
         "breakdown_ms": phase,
         "roofline": roof,
         "gpu_launches": int(launches),

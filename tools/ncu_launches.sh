@@ -1,7 +1,7 @@
 # per-launch device times of one bench step (cold-cache, serialised: compare shares)
 CFG=${1:-north_star}
 OUT=${2:-launches}
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/$OUT.csv python bench.py --config $CFG --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > /dev/null 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/$OUT.csv python bench.py --config $CFG --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-strong > /dev/null 2>&1
 python - "$OUT" <<'PY'
 import csv, sys, collections
 rows = list(csv.reader(open(f"gpurun_out/{sys.argv[1]}.csv")))
