@@ -1126,13 +1126,17 @@ __global__ void __launch_bounds__(kFinishWarps * 32, FG_FINISH_MINB) k_tile_fini
     // the next query's meta and list entries are loaded while this one is
     // finished (the list row is read whole, without waiting for its length):
     // only the coordinate / id gathers stay on the per-query critical path
+    // two-deep: the meta of query p + 2 stride and the list entries of query
+    // p + stride (only its m of them: the meta arrived an iteration earlier)
+    // load while query p is finished
     const int64_t stride = (int64_t)gridDim.x * kFinishWarps;
     int64_t p = blockIdx.x * (int64_t)kFinishWarps + (threadIdx.x >> 5);
     float2 mt = p < n ? a.meta[p] : make_float2(0.f, -1.f);
+    float2 mt_n = p + stride < n ? a.meta[p + stride] : make_float2(0.f, -1.f);
     int32_t lnext[kRounds];
 #pragma unroll
     for (int t = 0; t < kRounds; ++t)
-        lnext[t] = (p < n && lane + 32 * t < kCap) ? a.lists[p * kCap + lane + 32 * t] : -1;
+        lnext[t] = lane + 32 * t < (int)mt.y ? a.lists[p * kCap + lane + 32 * t] : -1;
     for (; p < n; p += stride) {
         const int m = (int)mt.y;
         const float tau_p = mt.x;
@@ -1140,11 +1144,13 @@ __global__ void __launch_bounds__(kFinishWarps * 32, FG_FINISH_MINB) k_tile_fini
         Q.m = m;
 #pragma unroll
         for (int t = 0; t < kRounds; ++t) Q.cpos[t] = lnext[t];
-        const int64_t pn = p + stride;
-        mt = pn < n ? a.meta[pn] : make_float2(0.f, -1.f);
+        const int64_t pn = p + stride, pnn = p + 2 * stride;
+        const int mn = (int)mt_n.y;
 #pragma unroll
         for (int t = 0; t < kRounds; ++t)
-            lnext[t] = (pn < n && lane + 32 * t < kCap) ? a.lists[pn * kCap + lane + 32 * t] : -1;
+            lnext[t] = lane + 32 * t < mn ? a.lists[pn * kCap + lane + 32 * t] : -1;
+        mt = mt_n;
+        mt_n = pnn < n ? a.meta[pnn] : make_float2(0.f, -1.f);
         if (m < 0) continue;  // already on the redo list
 #pragma unroll
         for (int t = 0; t < kRounds; ++t) {

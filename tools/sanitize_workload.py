@@ -38,6 +38,25 @@ def run(coords, off, k, d_bin, **kw):
     return c, rs, idx, d2
 
 
+def hd_cases():
+    """The high-dimensional / float64 tile kernels (fg_knn_hd.cuh)."""
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(5)
+    x10, _ = generate_dataset(3000, 10, splits=1, seed=4)
+    run(x10, np.array([0, 3000], np.int64), 64, 5)
+    x6, _ = generate_dataset(2000, 6, splits=2, seed=8)
+    off6 = np.array([0, 900, 2000], np.int64)
+    run(x6, off6, 16, 5, direction=torch.from_numpy(rng.integers(0, 4, 2000).astype(np.int8)).to(dev))
+    # float64 coordinates (exact keys from the float64 values), a mask and a radius
+    c64 = torch.from_numpy(x6).to(dev)
+    rs = torch.from_numpy(off6).to(dev)
+    nb = fg.compute_n_bins(1100, 16, 5)
+    bi, so, bb, mins, widths, sc = ops.bin_by_coordinates(c64, rs, 5, nb)
+    ops.binned_select_knn(c64, rs, bi, so, bb, mins, widths, sc, 16, 5, nb, None, 0.05, False, True)
+    ops.binned_select_knn(c64, rs, bi, so, bb, mins, widths, sc, 100, 5, nb, None, None, False, True)
+    torch.cuda.synchronize()
+
+
 def main():
     torch.manual_seed(0)
     rng = np.random.default_rng(1)
@@ -74,4 +93,8 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if "--hd" in sys.argv:
+        hd_cases()
+        print("sanitize hd workload done")
+    else:
+        main()
