@@ -8,7 +8,7 @@ using namespace fg::search;
 
 namespace fg {
 namespace tile {
-int launch(TileArgs& t, const search::KnnArgs& a, int d_bin, cudaStream_t st);
+int launch(TileArgs& t, const search::KnnArgs& a, int d_bin, cudaStream_t st, TileArgs* clustered);
 }
 namespace gravnet {
 int reducer_bits(const int32_t* reducers, int n_red, unsigned* bits);
@@ -17,6 +17,38 @@ int reducer_bits(const int32_t* reducers, int n_red, unsigned* bits);
 
 namespace {
 unsigned long long* g_stats_dev = nullptr;  // FG_KNN_STATS counters (lazily allocated)
+
+// Per-device host-mapped "the last tile-path call was clustered" flag (see
+// TileArgs::hint).  It only picks which exact path is launched; results are
+// identical either way.
+constexpr int kMaxDevices = 64;
+std::mutex g_hint_mu;
+volatile int* g_hint_host[kMaxDevices] = {};
+int* g_hint_dev[kMaxDevices] = {};
+
+int clustered_hint(int** dev_ptr, bool* last_clustered) {
+    int dev = 0;
+    FG_CUDA(cudaGetDevice(&dev));
+    *dev_ptr = nullptr;
+    *last_clustered = true;  // unknown: launch the (gated) fallback
+    if (dev < 0 || dev >= kMaxDevices) return 0;
+    std::lock_guard<std::mutex> lk(g_hint_mu);
+    if (!g_hint_host[dev]) {
+        int* h = nullptr;
+        if (cudaHostAlloc((void**)&h, sizeof(int), cudaHostAllocMapped) != cudaSuccess) {
+            cudaGetLastError();
+            return 0;
+        }
+        *h = 1;
+        int* d = nullptr;
+        FG_CUDA(cudaHostGetDevicePointer((void**)&d, h, 0));
+        g_hint_host[dev] = h;
+        g_hint_dev[dev] = d;
+    }
+    *dev_ptr = g_hint_dev[dev];
+    *last_clustered = *g_hint_host[dev] != 0;
+    return 0;
+}
 std::mutex g_stats_mu;
 constexpr int kStatsTotal = ST_COUNT + tile::TS_COUNT + hd::HS_COUNT;
 
@@ -77,6 +109,9 @@ struct TileWs {
     int* ctr;
     int2* tiles;
     int32_t* redo;
+    float4* sc2;     // hd path: search copies (dense cells in Morton order)
+    int32_t* sid2;
+    int32_t* dense;
     int32_t* lists;  // split epilogue: n * kCap sorted positions
     float2* meta;    //                 n * (tau, m)
     size_t bytes;
@@ -106,7 +141,7 @@ TileWs tile_ws(void* base, int64_t n, int32_t n_splits, int32_t d_bin, int32_t n
     w.bytes = off;
     return w;
 }
-TileWs hd_ws(void* base, int64_t n, int32_t n_splits, int32_t d_bin, int32_t n_bins) {
+TileWs hd_ws(void* base, int64_t n, int32_t n_coords, int32_t n_splits, int32_t d_bin, int32_t n_bins) {
     TileWs w{};
     const int64_t nblk = (n_bins + 1) / 2;
     int64_t bps = 1;
@@ -121,6 +156,14 @@ TileWs hd_ws(void* base, int64_t n, int32_t n_splits, int32_t d_bin, int32_t n_b
     off = align_up(off + sizeof(int2) * (size_t)max_tiles, 256);
     w.redo = reinterpret_cast<int32_t*>(p + off);
     off = align_up(off + sizeof(int32_t) * (size_t)std::max<int64_t>(n, 1), 256);
+    // the search's copies of the sorted coordinates / ids (dense cells re-ordered)
+    const int nv = (n_coords + 3) / 4;
+    w.sc2 = reinterpret_cast<float4*>(p + off);
+    off = align_up(off + sizeof(float4) * nv * (size_t)std::max<int64_t>(n, 1), 256);
+    w.sid2 = reinterpret_cast<int32_t*>(p + off);
+    off = align_up(off + sizeof(int32_t) * (size_t)std::max<int64_t>(n, 1), 256);
+    w.dense = reinterpret_cast<int32_t*>(p + off);
+    off = align_up(off + sizeof(int32_t) * (size_t)(n / (hd::kDenseCell + 1) + 1), 256);
     w.bytes = off;
     return w;
 }
@@ -131,9 +174,10 @@ extern "C" int fg_knn_workspace_size(int64_t n, int32_t n_coords, int32_t n_spli
     if (!bytes) return FG_ERR_NULL;
     if (n < 0 || n_splits < 1 || n_bins < 1) return FG_ERR_BAD_SHAPE;
     *bytes = tile_path(n_coords, n_splits, d_bin, n_bins, k, flags)
-                 ? tile_ws(nullptr, n, n_splits, d_bin, n_bins).bytes
+                 ? tile_ws(nullptr, n, n_splits, d_bin, n_bins).bytes +
+                       hd_ws(nullptr, n, n_coords, n_splits, d_bin, n_bins).bytes
                  : hd_path(n_coords, n_splits, d_bin, n_bins, k, flags)
-                       ? hd_ws(nullptr, n, n_splits, d_bin, n_bins).bytes
+                       ? hd_ws(nullptr, n, n_coords, n_splits, d_bin, n_bins).bytes
                        : 0;
     return 0;
 }
@@ -151,9 +195,10 @@ extern "C" int fg_knn_fwd(const float* sorted_coords, const int32_t* sort_order,
     if (n == 0) return 0;
     size_t bytes = 0;
     if (tile_path(n_coords, n_splits, d_bin, n_bins, k, flags))
-        bytes = tile_ws(nullptr, n, n_splits, d_bin, n_bins).bytes;
+        bytes = tile_ws(nullptr, n, n_splits, d_bin, n_bins).bytes +
+                hd_ws(nullptr, n, n_coords, n_splits, d_bin, n_bins).bytes;
     else if (hd_path(n_coords, n_splits, d_bin, n_bins, k, flags))
-        bytes = hd_ws(nullptr, n, n_splits, d_bin, n_bins).bytes;
+        bytes = hd_ws(nullptr, n, n_coords, n_splits, d_bin, n_bins).bytes;
     void* ws = nullptr;
     cudaStream_t st = (cudaStream_t)stream;
     if (bytes) FG_CUDA(cudaMallocAsync(&ws, bytes, st));
@@ -214,7 +259,9 @@ extern "C" int fg_knn_fwd_ws(const float* sorted_coords, const int32_t* sort_ord
     if (tile_path(n_coords, n_splits, d_bin, n_bins, k, flags)) {
         const TileWs w = tile_ws(workspace, n, n_splits, d_bin, n_bins);
         if (!workspace) return FG_ERR_NULL;
-        if (workspace_bytes < w.bytes) return FG_ERR_WORKSPACE;
+        const TileWs wh = hd_ws(static_cast<char*>(workspace) + w.bytes, n, n_coords, n_splits,
+                                d_bin, n_bins);
+        if (workspace_bytes < w.bytes + wh.bytes) return FG_ERR_WORKSPACE;
         tile::TileArgs t{};
         t.sc = a.sc;
         t.sid = sort_order;
@@ -237,10 +284,27 @@ extern "C" int fg_knn_fwd_ws(const float* sorted_coords, const int32_t* sort_ord
         t.lists = split ? w.lists : nullptr;
         t.meta = split ? w.meta : nullptr;
         t.stats = a.stats ? a.stats + ST_COUNT : nullptr;
-        return tile::launch(t, a, d_bin, st);
+        // the clustered-data fallback (high-dimensional tile kernels, gated on
+        // the tile kernels' decline rule on the device)
+        tile::TileArgs th = t;
+        th.tiles = wh.tiles;
+        th.ctr = wh.ctr;
+        th.redo = wh.redo;
+        th.lists = nullptr;
+        th.meta = nullptr;
+        th.sc2 = wh.sc2;
+        th.sid2 = wh.sid2;
+        th.dense = wh.dense;
+        th.stats = nullptr;
+        int* hint_dev = nullptr;
+        bool last_clustered = true;
+        FG_TRY(clustered_hint(&hint_dev, &last_clustered));
+        t.hint = hint_dev;
+        const bool fallback = !(flags & FG_KNN_NO_HD) && (last_clustered || !hint_dev);
+        return tile::launch(t, a, d_bin, st, fallback ? &th : nullptr);
     }
     if (hd_path(n_coords, n_splits, d_bin, n_bins, k, flags)) {
-        const TileWs w = hd_ws(workspace, n, n_splits, d_bin, n_bins);
+        const TileWs w = hd_ws(workspace, n, n_coords, n_splits, d_bin, n_bins);
         if (!workspace) return FG_ERR_NULL;
         if (workspace_bytes < w.bytes) return FG_ERR_WORKSPACE;
         tile::TileArgs t{};
@@ -261,6 +325,9 @@ extern "C" int fg_knn_fwd_ws(const float* sorted_coords, const int32_t* sort_ord
         t.redo = w.redo;
         t.out_idx = out_idx;
         t.stats = nullptr;
+        t.sc2 = w.sc2;
+        t.sid2 = w.sid2;
+        t.dense = w.dense;
         switch ((n_coords + 3) / 4) {
             case 1: return hd::dispatch_hd_nv1(t, a, d_bin, st);
             case 2: return hd::dispatch_hd_nv2(t, a, d_bin, st);
@@ -283,7 +350,7 @@ extern "C" int fg_knn_f64_workspace_size(int64_t n, int32_t n_coords, int32_t n_
     (void)flags;
     if (!bytes) return FG_ERR_NULL;
     if (n < 0 || n_splits < 1 || n_bins < 1) return FG_ERR_BAD_SHAPE;
-    *bytes = hd_ws(nullptr, n, n_splits, d_bin, n_bins).bytes + 256;
+    *bytes = hd_ws(nullptr, n, n_coords, n_splits, d_bin, n_bins).bytes + 256;
     return 0;
 }
 
@@ -301,7 +368,7 @@ extern "C" int fg_knn_fwd_f64_ws(const double* coords, const float* sorted_coord
     if (n == 0) return 0;
     if (!coords || !workspace) return FG_ERR_NULL;
     if (!hd_shape(n_splits, d_bin, n_bins, k)) return FG_ERR_UNSUPPORTED;
-    const TileWs w = hd_ws(workspace, n, n_splits, d_bin, n_bins);
+    const TileWs w = hd_ws(workspace, n, n_coords, n_splits, d_bin, n_bins);
     if (workspace_bytes < w.bytes + 256) return FG_ERR_WORKSPACE;
     unsigned* rnd = reinterpret_cast<unsigned*>(static_cast<char*>(workspace) + w.bytes);
     cudaStream_t st = (cudaStream_t)stream;
@@ -358,6 +425,9 @@ extern "C" int fg_knn_fwd_f64_ws(const double* coords, const float* sorted_coord
     t.ctr = w.ctr;
     t.redo = w.redo;
     t.out_idx = out_idx;
+    t.sc2 = w.sc2;
+    t.sid2 = w.sid2;
+    t.dense = w.dense;
     switch ((n_coords + 3) / 4) {
         case 1: return hd::dispatch_hd_nv1(t, a, d_bin, st);
         case 2: return hd::dispatch_hd_nv2(t, a, d_bin, st);

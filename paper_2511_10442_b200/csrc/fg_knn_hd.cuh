@@ -53,6 +53,10 @@ constexpr int kUnroll = FG_HD_UNROLL;  // 4-candidate groups in flight per chunk
 #define FG_HD_HINT_SCALE 0.5f
 #endif
 constexpr float kHintScale = FG_HD_HINT_SCALE;  // first-stage radius^2 / previous tile's
+#ifndef FG_HD_SEED
+#define FG_HD_SEED 256
+#endif
+constexpr int kSeed = FG_HD_SEED;  // stage-0 tau seeding window (sorted positions), 0: off
 #ifndef FG_HD_CAP
 #define FG_HD_CAP 128
 #endif
@@ -90,7 +94,7 @@ __global__ void __launch_bounds__(128) k_hd_tiles(const tile::TileArgs a) {
     constexpr int NL = DB - 1;
     const int lane = lane_id();
     const int blk = blockIdx.x * 4 + (threadIdx.x >> 5);
-    if (blk >= a.n_blocks) return;
+    if (blk >= a.n_blocks || tile::gated_off(a)) return;
     const int s = blk / a.bps;
     int o[NL > 0 ? NL : 1];
     tile::block_origin<NL>(blk - s * a.bps, a.nblk, o);
@@ -627,6 +631,39 @@ __global__ void __maxnreg__(224) k_hd_search(const __grid_constant__ tile::TileA
             tt = 0.0f;
         }
         int m = 0;
+        // cut every active lane holding >= keep entries to its keep smallest
+        auto tighten = [&]() {
+            unsigned todo = __ballot_sync(FG_FULL_MASK, active && m >= keep);
+            while (todo) {
+                const int j = __ffs(todo) - 1;
+                todo &= todo - 1;
+                const int mj = __shfl_sync(FG_FULL_MASK, m, j);
+                float qj[4 * NV];
+#pragma unroll
+                for (int d = 0; d < 4 * NV; ++d) qj[d] = __shfl_sync(FG_FULL_MASK, q[d], j);
+                const int32_t qidj = __shfl_sync(FG_FULL_MASK, qid, j);
+                const int rr = cut_lane<NV, X64, DE>(W, a, j, mj, keep, tau, tt, qj, qidj, r);
+                if (lane == j) m = rr;
+            }
+        };
+        const int32_t pmin_t = (int32_t)__reduce_min_sync(FG_FULL_MASK, (unsigned)(live ? p : 0x7fffffff));
+        const int32_t pmax_t = (int32_t)__reduce_max_sync(FG_FULL_MASK, (unsigned)(live ? p : 0));
+        if (kSeed > 0 && !use_r2 && pmax_t - pmin_t < 64) {  // the tile sits in a dense cell
+            // stage 0: tau seeds from the kSeed points around the tile's middle
+            // in the sorted order (same split) -- real points, so each lane's
+            // keep-th smallest among them bounds its answer; the entries are
+            // dropped (stage 1 rescans them) and only tau / tt are kept
+            const int64_t s_lo = a.rs[s], s_hi = a.rs[s + 1];
+            const int64_t mid = ((int64_t)pmin_t + pmax_t) / 2;
+            const int64_t w0 = max(s_lo, min(mid - kSeed / 2, s_hi - kSeed));
+            const int64_t w1 = min(s_hi, w0 + kSeed);
+            scan_spans<NV, DE, X64>(W, a, lane == 0 ? (int32_t)w0 : 0, lane == 0 ? (int32_t)(w1 - w0) : 0,
+                                    qd, tau, tt, m, keep, q, qid, r, bd_base, bp_base, st_chunks,
+                                    st_cuts);
+            tighten();
+            m = 0;
+            __syncwarp();
+        }
         // first stage at a fraction of the previous tile's radius: the nearest
         // rows come first, so the cuts tighten tau early (fewer appends later)
         float rho2 = rho2_hint * kHintScale;
@@ -675,19 +712,7 @@ __global__ void __maxnreg__(224) k_hd_search(const __grid_constant__ tile::TileA
                 scan_spans<NV, DE, X64>(W, a, S1, L1, qd, tau, tt, m, keep, q, qid, r, bd_base,
                                         bp_base, st_chunks, st_cuts);
             }
-            // tighten every lane to its keep-th smallest entry
-            unsigned todo = __ballot_sync(FG_FULL_MASK, active && m >= keep);
-            while (todo) {
-                const int j = __ffs(todo) - 1;
-                todo &= todo - 1;
-                const int mj = __shfl_sync(FG_FULL_MASK, m, j);
-                float qj[4 * NV];
-#pragma unroll
-                for (int d = 0; d < 4 * NV; ++d) qj[d] = __shfl_sync(FG_FULL_MASK, q[d], j);
-                const int32_t qidj = __shfl_sync(FG_FULL_MASK, qid, j);
-                const int rr = cut_lane<NV, X64, DE>(W, a, j, mj, keep, tau, tt, qj, qidj, r);
-                if (lane == j) m = rr;
-            }
+            tighten();  // every lane to its keep-th smallest entry
             const float need_t = tile::warp_max_f(active ? tt : 0.0f);
             prev = cur;
             // done when every lane's tt-ball is inside the region, or the region
@@ -786,15 +811,125 @@ static __global__ void k_abs_bound(const double* __restrict__ x, int64_t m, int 
     }
 }
 
+// ---------------------------------------------------------------- dense cells
+// Clustered data puts thousands of points in one cell; in the binning's order
+// (ascending id inside a cell) 32 consecutive points of such a cell are spread
+// over the whole cell, so a tile's box is the cell and its tau seeds are poor.
+// The search therefore runs on copies of the sorted coordinates / ids in which
+// the points of every cell with more than kDenseCell points are ordered by the
+// Morton code of their position inside the cell (cells stay contiguous ranges:
+// bin_bounds is unchanged; outputs are original ids, so the answer is the same).
+constexpr int kDenseCell = 32;
+constexpr int kMaxSortCell = 16384;  // larger cells keep the binning's order
+
+template <int NV>
+__global__ void __launch_bounds__(256) k_cell_split(const tile::TileArgs t, int64_t n_cells) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= n_cells || tile::gated_off(t)) return;
+    const int32_t lo = t.bounds[c], len = t.bounds[c + 1] - lo;
+    if (len > kDenseCell && len <= kMaxSortCell) {
+        t.dense[atomicAdd(&t.ctr[5], 1)] = (int32_t)c;
+        return;
+    }
+    for (int i = 0; i < len; ++i) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) t.sc2[(int64_t)(lo + i) * NV + v] = t.sc[(int64_t)(lo + i) * NV + v];
+        t.sid2[lo + i] = t.sid[lo + i];
+    }
+}
+
+__device__ __forceinline__ unsigned morton_spread(unsigned x, int dims, int bits) {
+    unsigned r = 0;
+    for (int b = 0; b < bits; ++b) r |= ((x >> b) & 1u) << (b * dims);
+    return r;
+}
+
+template <int NV, int DB>
+__global__ void __launch_bounds__(1024) k_dense_morton(const tile::TileArgs t) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    unsigned long long* key = reinterpret_cast<unsigned long long*>(smem_raw);  // (morton << 32) | i
+    constexpr int bits = 32 / DB > 10 ? 10 : 32 / DB;
+    if (tile::gated_off(t)) return;
+    const int count = t.ctr[5];
+    for (int it = blockIdx.x; it < count; it += gridDim.x) {
+        const int32_t c = t.dense[it];
+        const int32_t lo = t.bounds[c], len = t.bounds[c + 1] - lo;
+        const int64_t s = c / t.total;
+        int64_t flat = c - s * t.total;
+        int cell[DB];
+#pragma unroll
+        for (int i = DB - 1; i >= 0; --i) {
+            cell[i] = (int)(flat % t.nb);
+            flat /= t.nb;
+        }
+        int p2 = 64;
+        while (p2 < len) p2 <<= 1;
+        for (int i = threadIdx.x; i < p2; i += blockDim.x) {
+            unsigned long long kk = ~0ull;
+            if (i < len) {
+                const float4 x = t.sc[(int64_t)(lo + i) * NV];
+                const float xa[4] = {x.x, x.y, x.z, x.w};
+                unsigned mk = 0;
+#pragma unroll
+                for (int d = 0; d < DB && d < 4; ++d) {
+                    const double w = t.widths[s * DB + d];
+                    const double u = ((double)xa[d] - (t.mins[s * DB + d] + cell[d] * w)) / w;
+                    const int qd = min((1 << bits) - 1, max(0, (int)(u * (1 << bits))));
+                    mk |= morton_spread((unsigned)qd, DB, bits) << d;
+                }
+                kk = ((unsigned long long)mk << 32) | (unsigned)i;
+            }
+            key[i] = kk;
+        }
+        __syncthreads();
+        for (int size = 2; size <= p2; size <<= 1)
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                for (int i = threadIdx.x; i < p2 / 2; i += blockDim.x) {
+                    const int x0 = 2 * stride * (i / stride) + (i % stride), x1 = x0 + stride;
+                    const bool up = (x0 & size) == 0;
+                    const unsigned long long ka = key[x0], kb = key[x1];
+                    if ((ka > kb) == up) {
+                        key[x0] = kb;
+                        key[x1] = ka;
+                    }
+                }
+                __syncthreads();
+            }
+        for (int j = threadIdx.x; j < len; j += blockDim.x) {
+            const int src = (int)(key[j] & 0xffffffffu);
+#pragma unroll
+            for (int v = 0; v < NV; ++v) t.sc2[(int64_t)(lo + j) * NV + v] = t.sc[(int64_t)(lo + src) * NV + v];
+            t.sid2[lo + j] = t.sid[lo + src];
+        }
+        __syncthreads();
+    }
+}
+
 // Tile list, then the search (no redo: cuts fall back to exact keys).
 template <int NV, int DB, int DE, bool X64>
-int launch_hd(tile::TileArgs& t, const search::KnnArgs& a, cudaStream_t st) {
+int launch_hd(tile::TileArgs& t_in, const search::KnnArgs& a_in, cudaStream_t st) {
+    tile::TileArgs t = t_in;
+    search::KnnArgs a = a_in;
     FG_CUDA(cudaMemsetAsync(t.ctr, 0, 8 * sizeof(int), st));
     k_hd_tiles<DB><<<(unsigned)ceil_div(t.n_blocks, 4), 128, 0, st>>>(t);
     FG_TRY(launched(st));
     int dev = 0, sms = 0;
     FG_CUDA(cudaGetDevice(&dev));
     FG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (t.sc2) {  // dense cells in Morton order: the search's own copies of sc / sid
+        const int64_t n_cells = (int64_t)t.n_blocks / t.bps * t.total;
+        k_cell_split<NV><<<(unsigned)ceil_div(n_cells, 256), 256, 0, st>>>(t, n_cells);
+        FG_TRY(launched(st));
+        const size_t msmem = sizeof(unsigned long long) * kMaxSortCell;
+        FG_CUDA(cudaFuncSetAttribute(k_dense_morton<NV, DB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)msmem));
+        k_dense_morton<NV, DB><<<(unsigned)sms, 1024, msmem, st>>>(t);
+        FG_TRY(launched(st));
+        t.sc = t.sc2;
+        t.sid = t.sid2;
+        a.sc = t.sc2;
+        a.sid = t.sid2;
+    }
     constexpr size_t smem = hd_smem_bytes<DE>();
     auto kern = k_hd_search<NV, DB, DE, X64>;
     FG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -7,10 +7,14 @@ namespace search {
 int dispatch_nv1(const KnnArgs& a, int d_bin, cudaStream_t st) { return dispatch_db<1>(a, d_bin, st); }
 }  // namespace search
 
+namespace hd {
+int dispatch_hd_nv1(tile::TileArgs& t, const search::KnnArgs& a, int d_bin, cudaStream_t st);
+}
+
 namespace tile {
 
 template <int DB>
-int launch_db(TileArgs& t, const search::KnnArgs& a, cudaStream_t st) {
+int launch_db(TileArgs& t, const search::KnnArgs& a, cudaStream_t st, TileArgs* clustered) {
     FG_CUDA(cudaMemsetAsync(t.ctr, 0, 8 * sizeof(int), st));
     k_tiles<DB><<<(unsigned)ceil_div(t.n_blocks, 4), 128, 0, st>>>(t);
     FG_TRY(launched(st));
@@ -39,15 +43,23 @@ int launch_db(TileArgs& t, const search::KnnArgs& a, cudaStream_t st) {
     r.qlist = t.redo;
     r.qcount = &t.ctr[2];
     r.qall = &t.ctr[4];
+    if (clustered) {
+        // data the tile kernels declined (clustered at the cell scale): the
+        // high-dimensional tile kernels with dense cells in Morton order take
+        // every query instead of the warp-per-query kernel (gated on the device)
+        clustered->gate = &t.ctr[4];
+        FG_TRY(hd::dispatch_hd_nv1(*clustered, a, DB, st));
+        r.qall = nullptr;  // declined: the redo list is empty
+    }
     return search::dispatch_db<1>(r, DB, st);
 }
 
-int launch(TileArgs& t, const search::KnnArgs& a, int d_bin, cudaStream_t st) {
+int launch(TileArgs& t, const search::KnnArgs& a, int d_bin, cudaStream_t st, TileArgs* clustered) {
     switch (d_bin) {
-        case 1: return launch_db<1>(t, a, st);
-        case 2: return launch_db<2>(t, a, st);
-        case 3: return launch_db<3>(t, a, st);
-        default: return launch_db<4>(t, a, st);
+        case 1: return launch_db<1>(t, a, st, clustered);
+        case 2: return launch_db<2>(t, a, st, clustered);
+        case 3: return launch_db<3>(t, a, st, clustered);
+        default: return launch_db<4>(t, a, st, clustered);
     }
 }
 

@@ -93,7 +93,25 @@ struct TileArgs {
     // list (sorted positions, kCap per query) and (tau, m); k_tile_finish sorts
     int32_t* lists;
     float2* meta;
+    // high-dimensional path (fg_knn_hd.cuh): search copies of sc / sid with the
+    // points of dense cells in Morton order of their sub-cell position (null:
+    // the binning's order is used as is)
+    float4* sc2;
+    int32_t* sid2;
+    int32_t* dense;
+    // hd path as the clustered-data fallback of the d <= 4 tile path: run only
+    // when *gate * 4 > n (the tile kernels declined the data); null: always
+    const int* gate;
+    // host-mapped flag: the scan kernel records whether it declined the data,
+    // so the next call launches the (gated) fallback only when the data of
+    // the previous call was clustered (either way the answer is the same)
+    volatile int* hint;
 };
+
+// The hd kernels' gate (see TileArgs::gate).
+__device__ __forceinline__ bool gated_off(const TileArgs& a) {
+    return a.gate && (int64_t)*a.gate * 4 <= a.n;
+}
 
 // Per-warp shared memory of the scan.
 struct ScanWarp {
@@ -788,6 +806,7 @@ __global__ void __launch_bounds__(kWarps * 32, SPLIT ? kScanCtasPerSm : kCtasPer
     const int nb = a.nb;
     const int need = a.k - 1;
     const int n_tiles = tiles_declined(a) ? 0 : a.ctr[0];
+    if (a.hint && blockIdx.x == 0 && threadIdx.x == 0) *a.hint = tiles_declined(a) ? 1 : 0;
     unsigned long long st_cand = 0, st_tiles = 0, st_redo = 0, st_fail = 0, st_exp = 0, st_eval = 0;
 
     for (;;) {

@@ -1,0 +1,3 @@
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider -x --deselect tests/test_gpu_reference_suite.py 2>&1 | tail -3
+for c in B north_star; do for i in 1 2; do timeout 300 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --no-strong 2>/dev/null | python -c "import sys,json; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('$c', round(d['ms_per_step'],3), {k:round(v,3) for k,v in d['breakdown_ms'].items()})"; done; done
+timeout 300 python tools/hd_stats.py B 2>&1 | grep "B default"
