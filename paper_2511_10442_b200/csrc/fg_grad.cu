@@ -228,7 +228,10 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) k_knn_bwd_pipe(
 // and the TwoSum corrections (lo REDs) of row i-1 go out once their atomics
 // have returned.  The query side of a row (a warp sum, exactly one writer) is
 // stored, not accumulated: qside[v].  Same arithmetic as k_knn_bwd_pipe.
-constexpr int kBwdChunk = 64;  // rows per CTA chunk (k_knn_bwd_stream)
+#ifndef FG_BWD_CHUNK
+#define FG_BWD_CHUNK 64
+#endif
+constexpr int kBwdChunk = FG_BWD_CHUNK;  // rows per CTA chunk (k_knn_bwd_stream)
 
 struct BwdRow {
     int64_t v;

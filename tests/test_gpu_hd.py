@@ -108,3 +108,18 @@ def test_hd_config_c_sample():
     rs = torch.from_numpy(off).cuda()
     bi, bd = ops.brute_knn(ct, rs, k, torch.from_numpy(rows).cuda())
     assert_rows(gi[rows], gd[rows], bi.cpu().numpy(), bd.cpu().numpy(), "config C sample")
+
+
+@pytest.mark.parametrize("n,d,k,splits", [(60_000, 4, 40, 1), (30_000, 3, 16, 3), (20_000, 2, 12, 2)])
+def test_clustered_fallback_equals_warp_kernel(n, d, k, splits):
+    """d <= 4 clustered data: the tile path declines and the high-dimensional
+    tile kernels (dense cells in Morton order, stage-0 seeds) take every query;
+    bit-identical to the warp-per-query kernel and to the brute force."""
+    c, off = generate_dataset(n, d, splits, 7 + d, "clusters")
+    c32 = c.astype(np.float32)
+    gi, gd, st = search(c32, off, k, d, stats=True)
+    assert st["hd_tiles"] > 0, "the clustered fallback did not run"
+    wi, wd, _ = search(c32, off, k, d, flags=_lib.FG_KNN_NO_HD)
+    assert_rows(gi, gd, wi, wd, "clustered fallback vs warp-per-query")
+    bi, bd = brute(c32, off, k)
+    assert_rows(gi, gd, bi, bd.astype(np.float32), "clustered fallback vs brute")
