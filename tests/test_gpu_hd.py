@@ -117,6 +117,7 @@ def test_clustered_fallback_equals_warp_kernel(n, d, k, splits):
     bit-identical to the warp-per-query kernel and to the brute force."""
     c, off = generate_dataset(n, d, splits, 7 + d, "clusters")
     c32 = c.astype(np.float32)
+    search(c32, off, k, d)  # a clustered call: the next one launches the fallback
     gi, gd, st = search(c32, off, k, d, stats=True)
     assert st["hd_tiles"] > 0, "the clustered fallback did not run"
     wi, wd, _ = search(c32, off, k, d, flags=_lib.FG_KNN_NO_HD)
