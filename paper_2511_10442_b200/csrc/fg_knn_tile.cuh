@@ -119,7 +119,7 @@ struct ScanWarp {
     int32_t spS[kMaxSpans];               // span start (sorted position)
     uint16_t spE[kMaxSpans + 1];          // span flattened start (exclusive prefix)
     alignas(16) float sx[4][64];          // candidate ring (2 chunks), SoA (centred when expanded)
-    alignas(16) float sn[32];             // expanded mode: |c - centre|^2
+    alignas(16) float sn[64];             // expanded mode: |c - centre|^2 (ring)
     alignas(16) uint16_t scode[64];       // ring codes
 };
 // ... plus the epilogue staging when the scan kernel finishes its own queries
@@ -474,8 +474,10 @@ __device__ __forceinline__ void scan_tile(ScanWarp& W, const float4* __restrict_
 // (about half of the region's candidates at north_star: the region is built
 // at cell granularity).  Fetched chunks are compacted into a 64-entry ring and
 // evaluated 32 at a time, so the broadcast loop only sees useful candidates.
+template <bool EXP>
 __device__ __forceinline__ void scan_tile_filtered(ScanWarp& W, const float4* __restrict__ sc, int T,
-                                                   int nsp, const QP& qv, float tau,
+                                                   int nsp, const QP& qv, const QX& qx,
+                                                   const float4 cen, float tau,
                                                    const float4 blo, const float4 bhi, float thr,
                                                    uint32_t& ptr, bool& overflow, uint32_t llim,
                                                    unsigned long long& n_eval) {
@@ -524,10 +526,19 @@ __device__ __forceinline__ void scan_tile_filtered(ScanWarp& W, const float4* __
             const unsigned bal = __ballot_sync(FG_FULL_MASK, useful);
             if (useful) {
                 const int slot = (head + filled + __popc(bal & lanemask_lt())) & 63;
-                W.sx[0][slot] = c.x;
-                W.sx[1][slot] = c.y;
-                W.sx[2][slot] = c.z;
-                W.sx[3][slot] = c.w;
+                if (EXP) {  // centred on the tile box, with |c'|^2
+                    const float4 cc = make_float4(c.x - cen.x, c.y - cen.y, c.z - cen.z, c.w - cen.w);
+                    W.sx[0][slot] = cc.x;
+                    W.sx[1][slot] = cc.y;
+                    W.sx[2][slot] = cc.z;
+                    W.sx[3][slot] = cc.w;
+                    W.sn[slot] = fmaf(cc.w, cc.w, fmaf(cc.z, cc.z, fmaf(cc.y, cc.y, cc.x * cc.x)));
+                } else {
+                    W.sx[0][slot] = c.x;
+                    W.sx[1][slot] = c.y;
+                    W.sx[2][slot] = c.z;
+                    W.sx[3][slot] = c.w;
+                }
                 W.scode[slot] = (uint16_t)code;
             }
             filled += __popc(bal);
@@ -535,7 +546,12 @@ __device__ __forceinline__ void scan_tile_filtered(ScanWarp& W, const float4* __
         if (filled == 0) break;
         if (filled < 32 && lane >= filled) {  // last round: pad with far-away sentinels
             const int slot = (head + lane) & 63;
-            W.sx[0][slot] = kInf; W.sx[1][slot] = kInf; W.sx[2][slot] = kInf; W.sx[3][slot] = kInf;
+            if (EXP) {
+                W.sx[0][slot] = 0.f; W.sx[1][slot] = 0.f; W.sx[2][slot] = 0.f; W.sx[3][slot] = 0.f;
+                W.sn[slot] = kInf;
+            } else {
+                W.sx[0][slot] = kInf; W.sx[1][slot] = kInf; W.sx[2][slot] = kInf; W.sx[3][slot] = kInf;
+            }
         }
         __syncwarp();
         n_eval += 32;
@@ -551,15 +567,30 @@ __device__ __forceinline__ void scan_tile_filtered(ScanWarp& W, const float4* __
                 cd[8 * j + 2 * h + 1] = w4[h] >> 16;
             }
         }
-        G4 gb[2];
-        load_g4(gb[0], base, 0);
+        if (EXP) {  // |c'|^2 - 2 q'.c' against tau - |q'|^2: 4 FFMA2 per candidate pair
+            G4X gb[2];
+            load_g4x(gb[0], base, 0);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            if (j + 1 < 8) load_g4(gb[(j + 1) & 1], base, 4 * (j + 1));
-            eval_g4(gb[j & 1], qv, tau, ptr, cd[4 * j], cd[4 * j + 1], cd[4 * j + 2], cd[4 * j + 3]);
-            if ((j & 3) == 3 && ptr > llim) {  // clamp every 16 candidates (kSlack)
-                overflow = true;
-                ptr = llim;
+            for (int j = 0; j < 8; ++j) {
+                if (j + 1 < 8) load_g4x(gb[(j + 1) & 1], base, 4 * (j + 1));
+                eval_g4x(gb[j & 1], qx, qx.tau_x, ptr, cd[4 * j], cd[4 * j + 1], cd[4 * j + 2],
+                         cd[4 * j + 3]);
+                if ((j & 3) == 3 && ptr > llim) {
+                    overflow = true;
+                    ptr = llim;
+                }
+            }
+        } else {
+            G4 gb[2];
+            load_g4(gb[0], base, 0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (j + 1 < 8) load_g4(gb[(j + 1) & 1], base, 4 * (j + 1));
+                eval_g4(gb[j & 1], qv, tau, ptr, cd[4 * j], cd[4 * j + 1], cd[4 * j + 2], cd[4 * j + 3]);
+                if ((j & 3) == 3 && ptr > llim) {  // clamp every 16 candidates (kSlack)
+                    overflow = true;
+                    ptr = llim;
+                }
             }
         }
         __syncwarp();
@@ -1036,9 +1067,7 @@ __global__ void __launch_bounds__(kWarps * 32, SPLIT ? kScanCtasPerSm : kCtasPer
         qx.m2q[3] = pack2(-2.0f * qs.w);
         qx.tau_x = tau - sq;
         st_exp += expanded ? 1 : 0;
-        if (expanded) {
-            scan_tile<true>(W, a.sc, T, nsp, qv, qx, cen, tau, ptr, overflow, llim);
-        } else {
+        {
             float bl[4] = {0.f, 0.f, 0.f, 0.f}, bh[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int i = 0; i < DB; ++i) {  // the queries' physical bounding box
@@ -1046,7 +1075,13 @@ __global__ void __launch_bounds__(kWarps * 32, SPLIT ? kScanCtasPerSm : kCtasPer
                 bh[i] = warp_max_f(active ? qa[i] : -kInf);
             }
             const float thr = tau_max * kMargin + 1e-30f;
-            scan_tile_filtered(W, a.sc, T, nsp, qv, tau, make_float4(bl[0], bl[1], bl[2], bl[3]),
+            if (expanded)
+                scan_tile_filtered<true>(W, a.sc, T, nsp, qv, qx, cen, tau,
+                                         make_float4(bl[0], bl[1], bl[2], bl[3]),
+                                         make_float4(bh[0], bh[1], bh[2], bh[3]), thr, ptr, overflow,
+                                         llim, st_eval);
+            else
+            scan_tile_filtered<false>(W, a.sc, T, nsp, qv, qx, cen, tau, make_float4(bl[0], bl[1], bl[2], bl[3]),
                                make_float4(bh[0], bh[1], bh[2], bh[3]), thr, ptr, overflow, llim,
                                st_eval);
         }
