@@ -112,6 +112,8 @@ struct TileWs {
     float4* sc2;     // hd path: search copies (dense cells in Morton order)
     int32_t* sid2;
     int32_t* dense;
+    float4* boxes;   // hd path, d <= 4: per-32-position bounding boxes
+    uint8_t* tcnt;   // hd path: points per tile
     int32_t* lists;  // split epilogue: n * kCap sorted positions
     float2* meta;    //                 n * (tau, m)
     size_t bytes;
@@ -147,7 +149,9 @@ TileWs hd_ws(void* base, int64_t n, int32_t n_coords, int32_t n_splits, int32_t 
     int64_t bps = 1;
     for (int i = 0; i < d_bin - 1; ++i) bps *= nblk;
     w.n_blocks = bps * n_splits;
-    const int64_t max_tiles = n / 32 + w.n_blocks + 1;  // runs of 32 per block
+    // runs of <= 32 per block, a run never spanning more than hd::kTileSpan
+    // columns: at most one short run per column of a block
+    const int64_t max_tiles = n / 32 + w.n_blocks * n_bins + 1;
     char* p = static_cast<char*>(base);
     size_t off = 0;
     w.ctr = reinterpret_cast<int*>(p + off);
@@ -164,6 +168,13 @@ TileWs hd_ws(void* base, int64_t n, int32_t n_coords, int32_t n_splits, int32_t 
     off = align_up(off + sizeof(int32_t) * (size_t)std::max<int64_t>(n, 1), 256);
     w.dense = reinterpret_cast<int32_t*>(p + off);
     off = align_up(off + sizeof(int32_t) * (size_t)(n / (hd::kDenseCell + 1) + 1), 256);
+    w.tcnt = reinterpret_cast<uint8_t*>(p + off);
+    off = align_up(off + (size_t)max_tiles, 256);
+    w.boxes = nullptr;
+    if (n_coords <= hd::kFilterDE) {
+        w.boxes = reinterpret_cast<float4*>(p + off);
+        off = align_up(off + 2 * sizeof(float4) * (size_t)(n / 32 + 1), 256);
+    }
     w.bytes = off;
     return w;
 }
@@ -295,6 +306,8 @@ extern "C" int fg_knn_fwd_ws(const float* sorted_coords, const int32_t* sort_ord
         th.sc2 = wh.sc2;
         th.sid2 = wh.sid2;
         th.dense = wh.dense;
+        th.boxes = wh.boxes;
+        th.tcnt = wh.tcnt;
         th.stats = nullptr;
         int* hint_dev = nullptr;
         bool last_clustered = true;
@@ -328,6 +341,8 @@ extern "C" int fg_knn_fwd_ws(const float* sorted_coords, const int32_t* sort_ord
         t.sc2 = w.sc2;
         t.sid2 = w.sid2;
         t.dense = w.dense;
+        t.boxes = w.boxes;
+        t.tcnt = w.tcnt;
         switch ((n_coords + 3) / 4) {
             case 1: return hd::dispatch_hd_nv1(t, a, d_bin, st);
             case 2: return hd::dispatch_hd_nv2(t, a, d_bin, st);
@@ -428,6 +443,8 @@ extern "C" int fg_knn_fwd_f64_ws(const double* coords, const float* sorted_coord
     t.sc2 = w.sc2;
     t.sid2 = w.sid2;
     t.dense = w.dense;
+    t.boxes = w.boxes;
+    t.tcnt = w.tcnt;
     switch ((n_coords + 3) / 4) {
         case 1: return hd::dispatch_hd_nv1(t, a, d_bin, st);
         case 2: return hd::dispatch_hd_nv2(t, a, d_bin, st);

@@ -54,13 +54,20 @@ constexpr int kUnroll = FG_HD_UNROLL;  // 4-candidate groups in flight per chunk
 #endif
 constexpr float kHintScale = FG_HD_HINT_SCALE;  // first-stage radius^2 / previous tile's
 #ifndef FG_HD_SEED
-#define FG_HD_SEED 256
+#define FG_HD_SEED 248
 #endif
 constexpr int kSeed = FG_HD_SEED;  // stage-0 tau seeding window (sorted positions), 0: off
+static_assert(kSeed < 256, "8-bit seed bucket counters");
 #ifndef FG_HD_CAP
 #define FG_HD_CAP 128
 #endif
 constexpr int kCap = FG_HD_CAP;  // per-lane buffer entries
+#ifndef FG_HD_FILTER_DE
+#define FG_HD_FILTER_DE 4
+#endif
+// candidates are filtered against the tile's query box for DE <= this (the
+// clustered d <= 4 fallback: dense cells are scanned whole at cell granularity)
+constexpr int kFilterDE = FG_HD_FILTER_DE;
 constexpr int kStride = kCap + 1;
 constexpr int kMaxNeed1 = 64;  // host eligibility (float32 coordinates): k <= 64
 constexpr int kMaxK64 = kCap - 8;  // float64 coordinates: k <= 120 (a cut frees >= 4 slots)
@@ -69,14 +76,16 @@ constexpr float kTiny = 1e-35f;
 constexpr float kSlackCells = 1e-4f;
 constexpr float kInf = __builtin_huge_valf();
 
-enum { HS_TILES, HS_CHUNKS, HS_STAGES, HS_REDO, HS_COMPACT, HS_COUNT };  // HS_REDO: unused (no redo)
+enum { HS_TILES, HS_CHUNKS, HS_STAGES, HS_MAXCYC, HS_COMPACT, HS_COUNT };  // HS_MAXCYC: slowest tile (clock64)
 
 template <int DE>
 struct HdWarp {
     float bd[32 * kStride];    // lane buffers: fp32 d2 (odd stride: appends spread over banks)
     int32_t bp[32 * kStride];  //               sorted positions
-    alignas(16) float sx[DE][32];  // one 32-candidate chunk, SoA
-    alignas(16) int32_t spos[32];
+    // candidates, SoA: a 64-entry ring when filtered, else one 32-candidate
+    // chunk (at DE = 10 the extra 2.6 KB per warp would cost a CTA per SM)
+    alignas(16) float sx[DE][DE <= kFilterDE ? 64 : 32];
+    alignas(16) int32_t spos[DE <= kFilterDE ? 64 : 32];
     int32_t span_s[64], span_l[64];
     search::WarpBuf<128> eb;   // epilogue scratch (the warp-per-query kernel's)
 };
@@ -88,7 +97,13 @@ __host__ __device__ constexpr size_t hd_smem_bytes() {
 
 // ---------------------------------------------------------------- tile list
 // One warp per (split, lead block): lane c owns last-dim column c (nb <= 32);
-// the block's points in (column, row) order are cut into runs of 32.
+// the block's points in (column, row) order are cut into runs of <= 32 that
+// never span more than kTileSpan columns: in a sparse block 32 consecutive
+// points can lie in columns far apart, and a tile's region is the union of
+// its queries' -- one elongated tile then scans most of the split (config B:
+// a single such tile took 2 ms).
+constexpr int kTileSpan = 2;
+
 template <int DB>
 __global__ void __launch_bounds__(128) k_hd_tiles(const tile::TileArgs a) {
     constexpr int NL = DB - 1;
@@ -117,12 +132,45 @@ __global__ void __launch_bounds__(128) k_hd_tiles(const tile::TileArgs a) {
             }
         }
     }
-    const int T = __reduce_add_sync(FG_FULL_MASK, col);
-    const int nt = (T + 31) >> 5;
+    // the cut (warp-uniform walk over the columns): pass 0 counts, pass 1 writes
     int t0 = 0;
-    if (lane == 0 && nt > 0) t0 = atomicAdd(&a.ctr[0], nt);
-    t0 = __shfl_sync(FG_FULL_MASK, t0, 0);
-    for (int i = lane; i < nt; i += 32) a.tiles[t0 + i] = make_int2(blk, 32 * i);
+    for (int pass = 0; pass < 2; ++pass) {
+        int nt = 0, run = 0, c0 = 0, g0 = 0, g = 0;
+        auto emit = [&](int start, int len) {
+            if (pass == 1 && lane == 0) {
+                a.tiles[t0 + nt] = make_int2(blk, start);
+                a.tcnt[t0 + nt] = (uint8_t)len;
+            }
+            ++nt;
+        };
+        for (int c = 0; c < nb; ++c) {
+            int cnt = __shfl_sync(FG_FULL_MASK, col, c);
+            if (cnt == 0) continue;
+            if (run > 0 && c - c0 >= kTileSpan) {
+                emit(g0, run);
+                run = 0;
+            }
+            while (cnt > 0) {
+                if (run == 0) {
+                    c0 = c;
+                    g0 = g;
+                }
+                const int take = min(cnt, 32 - run);
+                run += take;
+                cnt -= take;
+                g += take;
+                if (run == 32) {
+                    emit(g0, run);
+                    run = 0;
+                }
+            }
+        }
+        if (run > 0) emit(g0, run);
+        if (pass == 0) {
+            if (lane == 0 && nt > 0) t0 = atomicAdd(&a.ctr[0], nt);
+            t0 = __shfl_sync(FG_FULL_MASK, t0, 0);
+        }
+    }
 }
 
 // ---------------------------------------------------------------- helpers
@@ -350,14 +398,90 @@ __device__ __noinline__ int cut_lane(HdWarp<DE>& W, const search::KnnArgs& a, in
     return wpos;
 }
 
+// Stage-0 seed bound without buffers: every lane forms the fp32 d2 of the n
+// sorted positions from w0 (n <= 255, real points of the split) and counts
+// them in 32 quarter-octave buckets of x = d2 * s16 (8-bit counters packed in
+// four registers; bucket 0: x < 1, bucket 31: unbounded).  Returns an upper
+// bound of the lane's keep-th smallest d2 among them (the upper edge of the
+// bucket where the count reaches keep; the largest d2 if only the open bucket
+// does; +inf with fewer than keep points) -- within 25% of the value.
+template <int NV, int DE>
+__device__ __forceinline__ float seed_bound(HdWarp<DE>& W, const search::KnnArgs& a, int64_t w0, int n,
+                                            const unsigned long long (&qd)[DE], int keep, float s16) {
+    const int lane = lane_id();
+    const bool use_dir = a.flags & FG_KNN_USE_DIRECTION;
+    unsigned long long c[4] = {0ull, 0ull, 0ull, 0ull};
+    float mx = 0.0f;
+    int total = 0;
+    for (int f0 = 0; f0 < n; f0 += 32) {
+        int32_t cpos = f0 + lane < n ? (int32_t)(w0 + f0 + lane) : -1;
+        if (use_dir && cpos >= 0) {
+            const int8_t role = a.dir[a.sid[cpos]];
+            if (role == 1 || role == 2) cpos = -1;
+        }
+        if (cpos >= 0) {
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                const float4 x = a.sc[(int64_t)cpos * NV + v];
+                if (4 * v + 0 < DE) W.sx[4 * v + 0][lane] = x.x;
+                if (4 * v + 1 < DE) W.sx[4 * v + 1][lane] = x.y;
+                if (4 * v + 2 < DE) W.sx[4 * v + 2][lane] = x.z;
+                if (4 * v + 3 < DE) W.sx[4 * v + 3][lane] = x.w;
+            }
+        } else {
+#pragma unroll
+            for (int d = 0; d < DE; ++d) W.sx[d][lane] = kInf;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+            unsigned long long acc;
+#pragma unroll
+            for (int d = 0; d < DE; ++d) {
+                unsigned long long t0;
+                const unsigned long long cv = *reinterpret_cast<const unsigned long long*>(&W.sx[d][j]);
+                asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(t0) : "l"(qd[d]), "l"(cv));
+                if (d == 0) asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(acc) : "l"(t0));
+                else asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(acc) : "l"(t0), "l"(acc));
+            }
+            float dv[2];
+            asm("mov.b64 {%0, %1}, %2;" : "=f"(dv[0]), "=f"(dv[1]) : "l"(acc));
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                if (dv[u] < kInf) {
+                    const int key = (int)(__float_as_uint(dv[u] * s16) >> 21);
+                    const int b = min(max(key - 507, 0), 31);
+                    const unsigned long long inc = 1ull << ((b & 7) * 8);
+                    c[0] += (b >> 3) == 0 ? inc : 0ull;
+                    c[1] += (b >> 3) == 1 ? inc : 0ull;
+                    c[2] += (b >> 3) == 2 ? inc : 0ull;
+                    c[3] += (b >> 3) == 3 ? inc : 0ull;
+                    mx = fmaxf(mx, dv[u]);
+                    ++total;
+                }
+            }
+        }
+        __syncwarp();
+    }
+    if (total < keep) return kInf;
+    int cum = 0;
+#pragma unroll
+    for (int b = 0; b < 31; ++b) {
+        cum += (int)((c[b >> 3] >> ((b & 7) * 8)) & 0xffu);
+        if (cum >= keep)  // x < the bucket's upper edge
+            return fminf(mx, __uint_as_float((unsigned)(508 + b) << 21) / s16);
+    }
+    return mx;
+}
+
 // Evaluate one 32-candidate chunk (W.sx / W.spos) against every lane's query
 // and append the passing entries to the lanes' buffers.
 template <int DE, class Room>
-__device__ __forceinline__ void eval_chunk(HdWarp<DE>& W, const unsigned long long (&qd)[DE], int nlive,
+__device__ __forceinline__ void eval_chunk(HdWarp<DE>& W, const unsigned long long (&qd)[DE], int head,
                                            float& tau, uint32_t bd_base, uint32_t bp_base, int& m,
                                            Room&& room) {
-    const uint32_t sp_addr = (uint32_t)__cvta_generic_to_shared(&W.spos[0]);
-    (void)nlive;  // dead candidates carry +inf coordinates and position -1
+    // ring slots [head, head + 32); dead candidates carry +inf coordinates and position -1
+    const uint32_t sp_addr = (uint32_t)__cvta_generic_to_shared(&W.spos[head]);
     // phase 1: all 32 distances (straight-line FADD2/FFMA2 chains: full ILP)
     float dv[32];
 #pragma unroll
@@ -366,7 +490,7 @@ __device__ __forceinline__ void eval_chunk(HdWarp<DE>& W, const unsigned long lo
 #pragma unroll
         for (int d = 0; d < DE; ++d) {
             unsigned long long t0, t1;
-            const ulonglong2 cv = *reinterpret_cast<const ulonglong2*>(&W.sx[d][j]);
+            const ulonglong2 cv = *reinterpret_cast<const ulonglong2*>(&W.sx[d][head + j]);
             asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(t0) : "l"(qd[d]), "l"(cv.x));
             asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(t1) : "l"(qd[d]), "l"(cv.y));
             if (d == 0) {
@@ -411,38 +535,42 @@ __device__ __forceinline__ void eval_chunk(HdWarp<DE>& W, const unsigned long lo
     }
 }
 
-// Scan the given spans (one per lane) in 32-candidate chunks.
+// Candidate ring of the filtered scan: survivors of the query-box filter wait
+// here until 32 are ready (carried across scan_spans calls; flushed at the end
+// of a stage).
+struct Ring {
+    int head = 0, filled = 0;
+};
+
+// Scan the given spans (one per lane) in 32-candidate chunks.  DE <= kFilterDE:
+// spans are cut into pieces at 32-position block boundaries, pieces whose
+// block bounding box (boxes) lies farther than sqrt(max_l tau_l) from the
+// tile's query box are skipped, the remaining candidates are filtered one by
+// one against the query box and the survivors go through the ring; `final`
+// evaluates what is left in the ring.
 template <int NV, int DE, bool X64>
 __device__ __forceinline__ void scan_spans(HdWarp<DE>& W, const search::KnnArgs& a, int32_t S, int32_t L,
                                            const unsigned long long (&qd)[DE], float& tau, float& tt,
                                            int& m, int keep, const float (&q)[4 * NV], int32_t qid,
                                            float r, uint32_t bd_base, uint32_t bp_base,
+                                           const float (&qlo)[DE], const float (&qhi)[DE],
+                                           const float4* __restrict__ boxes, Ring& ring, bool final,
                                            unsigned long long& chunks, unsigned long long& cuts) {
+    constexpr bool FILT = DE <= kFilterDE;
     const int lane = lane_id();
     const unsigned nonempty = __ballot_sync(FG_FULL_MASK, L > 0);
-    if (!nonempty) return;
+    if (!nonempty && !(FILT && final && ring.filled > 0)) return;
     const bool use_dir = a.flags & FG_KNN_USE_DIRECTION;
-    const int ns = __popc(nonempty);
-    if (L > 0) {
-        const int dst = __popc(nonempty & lanemask_lt());
-        W.span_s[dst] = S;
-        W.span_l[dst] = L;
-    }
-    __syncwarp();
-    S = lane < ns ? W.span_s[lane] : 0;
-    L = lane < ns ? W.span_l[lane] : 0;
-    __syncwarp();
-    const int32_t incl = warp_inclusive_scan(L);
-    const int32_t excl = incl - L;
-    const int32_t T = __shfl_sync(FG_FULL_MASK, incl, 31);
     const unsigned le = (2u << lane) - 1u;
-    // candidate f -> sorted position (span flattening: one ballot + one redux)
-    auto pos_of = [&](int32_t f0) -> int32_t {
-        const int base = __popc(__ballot_sync(FG_FULL_MASK, lane < ns && incl <= f0));
+    // candidate f of a list of (start, length) runs held one per lane (nr
+    // lanes, inclusive / exclusive prefix of the lengths) -> sorted position
+    // (one ballot + one redux per 32 candidates)
+    auto pos_in = [&](int32_t f0, int nr, int32_t Sr, int32_t incl, int32_t excl, int32_t T) -> int32_t {
+        const int base = __popc(__ballot_sync(FG_FULL_MASK, lane < nr && incl <= f0));
         const unsigned starts = __reduce_or_sync(
-            FG_FULL_MASK, (lane < ns && excl > f0 && excl < f0 + 32) ? 1u << (excl - f0) : 0u);
+            FG_FULL_MASK, (lane < nr && excl > f0 && excl < f0 + 32) ? 1u << (excl - f0) : 0u);
         const int sidx = min(base + __popc(starts & le), 31);
-        const int32_t Ss = __shfl_sync(FG_FULL_MASK, S, sidx);
+        const int32_t Ss = __shfl_sync(FG_FULL_MASK, Sr, sidx);
         const int32_t Es = __shfl_sync(FG_FULL_MASK, excl, sidx);
         const int32_t f = f0 + lane;
         int32_t cpos = f < T ? Ss + (f - Es) : -1;
@@ -459,10 +587,6 @@ __device__ __forceinline__ void scan_spans(HdWarp<DE>& W, const search::KnnArgs&
             for (int v = 0; v < NV; ++v) x[v] = src[v];
         }
     };
-    // chunk f0 + 32 is loaded into registers while chunk f0 is evaluated
-    int32_t cpos_n = pos_of(0);
-    float4 xn[NV];
-    fetch(cpos_n, xn);
     // cut every lane whose buffer cannot take 4 more entries (warp-uniform)
     auto room = [&]() {
         unsigned full = __ballot_sync(FG_FULL_MASK, m > kCap - 4);
@@ -479,9 +603,147 @@ __device__ __forceinline__ void scan_spans(HdWarp<DE>& W, const search::KnnArgs&
             if (lane == j) m = rr;
         }
     };
+    // the runs in lanes [0, ns)
+    const int ns = __popc(nonempty);
+    if (L > 0) {
+        const int dst = __popc(nonempty & lanemask_lt());
+        W.span_s[dst] = S;
+        W.span_l[dst] = L;
+    }
+    __syncwarp();
+    S = lane < ns ? W.span_s[lane] : 0;
+    L = lane < ns ? W.span_l[lane] : 0;
+    __syncwarp();
+    if constexpr (FILT) {
+        auto coord = [](const float4 (&x)[NV], int d) -> float {
+            return d % 4 == 0 ? x[d / 4].x : d % 4 == 1 ? x[d / 4].y : d % 4 == 2 ? x[d / 4].z : x[d / 4].w;
+        };
+        auto thr_now = [&]() {
+            return __uint_as_float(__reduce_max_sync(FG_FULL_MASK, __float_as_uint(fmaxf(tau, 0.0f)))) *
+                       kMargin + kTiny;
+        };
+        auto eval_ring = [&]() {
+            __syncwarp();
+            ++chunks;
+            eval_chunk<DE>(W, qd, ring.head, tau, bd_base, bp_base, m, room);
+            __syncwarp();
+            ring.head ^= 32;
+            ring.filled -= 32;
+        };
+        // runs (Sr, Lr) in lanes [0, nr): filter every candidate against the
+        // query box, survivors into the ring, full chunks evaluated (the next
+        // 32 candidates' coordinates are loaded while a chunk is filtered)
+        auto consume = [&](int nr, int32_t Sr, int32_t Lr) {
+            const int32_t incl = warp_inclusive_scan(Lr);
+            const int32_t excl = incl - Lr;
+            const int32_t T = __shfl_sync(FG_FULL_MASK, incl, 31);
+            if (T == 0) return;
+            int32_t cn = pos_in(0, nr, Sr, incl, excl, T);
+            float4 xn[NV];
+            fetch(cn, xn);
+            for (int32_t f0 = 0; f0 < T; f0 += 32) {
+                const int32_t cpos = cn;
+                float4 x[NV];
+#pragma unroll
+                for (int v = 0; v < NV; ++v) x[v] = xn[v];
+                if (f0 + 32 < T) {
+                    cn = pos_in(f0 + 32, nr, Sr, incl, excl, T);
+                    fetch(cn, xn);
+                }
+                const float thr = thr_now();
+                float dd = 0.0f;
+#pragma unroll
+                for (int d = 0; d < DE; ++d) {
+                    const float xv = coord(x, d);
+                    const float gd = fmaxf(fmaxf(qlo[d] - xv, xv - qhi[d]), 0.0f);
+                    dd = fmaf(gd, gd, dd);
+                }
+                const bool useful = cpos >= 0 && dd <= thr;
+                const unsigned bal = __ballot_sync(FG_FULL_MASK, useful);
+                if (useful) {
+                    const int slot = (ring.head + ring.filled + __popc(bal & lanemask_lt())) & 63;
+#pragma unroll
+                    for (int d = 0; d < DE; ++d) W.sx[d][slot] = coord(x, d);
+                    W.spos[slot] = cpos;
+                }
+                ring.filled += __popc(bal);
+                if (ring.filled >= 32) eval_ring();
+            }
+        };
+        if (ns > 0) {
+            if (boxes) {
+                // pieces: the runs cut at 32-position block boundaries
+                const int np = L > 0 ? ((S + L - 1) >> 5) - (S >> 5) + 1 : 0;
+                const int32_t pin = warp_inclusive_scan(np);
+                const int32_t pex = pin - np;
+                const int32_t NP = __shfl_sync(FG_FULL_MASK, pin, 31);
+                for (int32_t pb = 0; pb < NP; pb += 32) {
+                    const int base = __popc(__ballot_sync(FG_FULL_MASK, lane < ns && pin <= pb));
+                    const unsigned starts = __reduce_or_sync(
+                        FG_FULL_MASK, (lane < ns && pex > pb && pex < pb + 32) ? 1u << (pex - pb) : 0u);
+                    const int sidx = min(base + __popc(starts & le), 31);
+                    const int32_t Ss = __shfl_sync(FG_FULL_MASK, S, sidx);
+                    const int32_t Ls = __shfl_sync(FG_FULL_MASK, L, sidx);
+                    const int32_t Ps = __shfl_sync(FG_FULL_MASK, pex, sidx);
+                    const int32_t f = pb + lane;
+                    const float thr = thr_now();
+                    int32_t ps = 0, pl = 0;
+                    if (f < NP) {
+                        const int32_t blk = (Ss >> 5) + (f - Ps);
+                        ps = max(Ss, blk << 5);
+                        pl = min(Ss + Ls, (blk << 5) + 32) - ps;
+                        const float4 blo = boxes[2 * blk], bhi = boxes[2 * blk + 1];
+                        const float bl[4] = {blo.x, blo.y, blo.z, blo.w}, bh[4] = {bhi.x, bhi.y, bhi.z, bhi.w};
+                        float dd = 0.0f;
+#pragma unroll
+                        for (int d = 0; d < DE; ++d) {
+                            const float gd = fmaxf(fmaxf(bl[d] - qhi[d], qlo[d] - bh[d]), 0.0f);
+                            dd = fmaf(gd, gd, dd);
+                        }
+                        if (!(dd <= thr)) pl = 0;
+                    }
+                    const unsigned keep_b = __ballot_sync(FG_FULL_MASK, pl > 0);
+                    if (!keep_b) continue;
+                    if (pl > 0) {
+                        const int dst = __popc(keep_b & lanemask_lt());
+                        W.span_s[32 + dst] = ps;
+                        W.span_l[32 + dst] = pl;
+                    }
+                    __syncwarp();
+                    const int nk = __popc(keep_b);
+                    const int32_t PS = lane < nk ? W.span_s[32 + lane] : 0;
+                    const int32_t PL = lane < nk ? W.span_l[32 + lane] : 0;
+                    __syncwarp();
+                    consume(nk, PS, PL);
+                }
+            } else {
+                consume(ns, S, L);
+            }
+        }
+        if (final && ring.filled > 0) {  // the rest, padded with dead sentinels
+            if (lane >= ring.filled) {
+                const int slot = (ring.head + lane) & 63;
+#pragma unroll
+                for (int d = 0; d < DE; ++d) W.sx[d][slot] = kInf;
+                W.spos[slot] = -1;
+            }
+            eval_ring();
+            ring.filled = 0;
+        }
+        return;
+    }
+    (void)boxes;
+    (void)final;
+    const int32_t incl = warp_inclusive_scan(L);
+    const int32_t excl = incl - L;
+    const int32_t T = __shfl_sync(FG_FULL_MASK, incl, 31);
+    auto pos_of = [&](int32_t f0) { return pos_in(f0, ns, S, incl, excl, T); };
+    // chunk f0 + 32 is loaded into registers while chunk f0 is evaluated
+    int32_t cpos_n = pos_of(0);
+    float4 xn[NV];
+    fetch(cpos_n, xn);
     for (int32_t f0 = 0; f0 < T; f0 += 32) {
         ++chunks;
-        const int nlive = min(32, T - f0);
         const int32_t cpos = cpos_n;
         if (cpos >= 0) {
 #pragma unroll
@@ -501,7 +763,7 @@ __device__ __forceinline__ void scan_spans(HdWarp<DE>& W, const search::KnnArgs&
             fetch(cpos_n, xn);
         }
         __syncwarp();
-        eval_chunk<DE>(W, qd, nlive, tau, bd_base, bp_base, m, room);
+        eval_chunk<DE>(W, qd, 0, tau, bd_base, bp_base, m, room);
         __syncwarp();
     }
 }
@@ -535,8 +797,9 @@ __global__ void __maxnreg__(224) k_hd_search(const __grid_constant__ tile::TileA
         ti = __shfl_sync(FG_FULL_MASK, ti, 0);
         if (ti >= n_tiles) break;
         ++st_tiles;
+        const long long tile_c0 = clock64();
         const int2 td = t.tiles[ti];
-        const int blk = td.x, start = td.y;
+        const int blk = td.x, start = td.y, tlen = t.tcnt[ti];
         const int s = blk / t.bps;
         int o[NL > 0 ? NL : 1];
         tile::block_origin<NL>(blk - s * t.bps, t.nblk, o);
@@ -568,7 +831,7 @@ __global__ void __maxnreg__(224) k_hd_search(const __grid_constant__ tile::TileA
         const int Ptot = __shfl_sync(FG_FULL_MASK, P, 31);
         const int Pprev = __shfl_sync(FG_FULL_MASK, P, max(c - 1, 0));
         int32_t p = -1;
-        if (g < Ptot && c < nb) {
+        if (lane < tlen && g < Ptot && c < nb) {
             int off = g - (c > 0 ? Pprev : 0);
             for (int rr = 0; rr < (1 << NL); ++rr) {
                 int rowflat = 0;
@@ -606,6 +869,7 @@ __global__ void __maxnreg__(224) k_hd_search(const __grid_constant__ tile::TileA
         unsigned long long qd[DE];
 #pragma unroll
         for (int d = 0; d < DE; ++d) qd[d] = dup2(q[d]);
+        float qlo[DE], qhi[DE];  // the unfinished queries' box (candidate filter, per stage)
         float w[DB], invw[DB], lo[DB], hi[DB];
         float diag2 = 0.0f;  // squared diagonal of the split's grid box
         float slack = kSlackCells;
@@ -631,9 +895,10 @@ __global__ void __maxnreg__(224) k_hd_search(const __grid_constant__ tile::TileA
             tt = 0.0f;
         }
         int m = 0;
+        bool done = false;  // the lane's answer is complete (region covers its tt-ball)
         // cut every active lane holding >= keep entries to its keep smallest
         auto tighten = [&]() {
-            unsigned todo = __ballot_sync(FG_FULL_MASK, active && m >= keep);
+            unsigned todo = __ballot_sync(FG_FULL_MASK, active && !done && m >= keep);
             while (todo) {
                 const int j = __ffs(todo) - 1;
                 todo &= todo - 1;
@@ -648,20 +913,27 @@ __global__ void __maxnreg__(224) k_hd_search(const __grid_constant__ tile::TileA
         };
         const int32_t pmin_t = (int32_t)__reduce_min_sync(FG_FULL_MASK, (unsigned)(live ? p : 0x7fffffff));
         const int32_t pmax_t = (int32_t)__reduce_max_sync(FG_FULL_MASK, (unsigned)(live ? p : 0));
-        if (kSeed > 0 && !use_r2 && pmax_t - pmin_t < 64) {  // the tile sits in a dense cell
+        if (kSeed > 0 && !use_r2) {
             // stage 0: tau seeds from the kSeed points around the tile's middle
             // in the sorted order (same split) -- real points, so each lane's
-            // keep-th smallest among them bounds its answer; the entries are
-            // dropped (stage 1 rescans them) and only tau / tt are kept
+            // keep-th smallest among them bounds its answer (bucketed: no
+            // buffers, no cuts)
             const int64_t s_lo = a.rs[s], s_hi = a.rs[s + 1];
             const int64_t mid = ((int64_t)pmin_t + pmax_t) / 2;
             const int64_t w0 = max(s_lo, min(mid - kSeed / 2, s_hi - kSeed));
             const int64_t w1 = min(s_hi, w0 + kSeed);
-            scan_spans<NV, DE, X64>(W, a, lane == 0 ? (int32_t)w0 : 0, lane == 0 ? (int32_t)(w1 - w0) : 0,
-                                    qd, tau, tt, m, keep, q, qid, r, bd_base, bp_base, st_chunks,
-                                    st_cuts);
-            tighten();
-            m = 0;
+            float bx = 0.0f;  // squared diagonal of the active queries' box: the bucket scale
+#pragma unroll
+            for (int d = 0; d < DE; ++d) {
+                const float e = tile::warp_max_f(active ? q[d] : -kInf) - tile::warp_min_f(active ? q[d] : kInf);
+                bx = fmaf(e, e, bx);
+            }
+            const float s16 = 16.0f / fmaxf(bx, 1e-30f);
+            const float b = seed_bound<NV, DE>(W, a, w0, (int)(w1 - w0), qd, keep, s16);
+            if (active && b < kInf) {
+                tt = fminf(tt, X64 ? up_bound(b, r) : b * kMargin + kTiny);
+                tau = X64 ? up_bound(tt, r) : tt;
+            }
             __syncwarp();
         }
         // first stage at a fraction of the previous tile's radius: the nearest
@@ -675,8 +947,20 @@ __global__ void __maxnreg__(224) k_hd_search(const __grid_constant__ tile::TileA
         }
         rho2 = fminf(rho2, diag2);
         Box<NL> prev = make_box<DB>(-1.0f, lo, hi, invw, nb, slack);
+        Ring ring;
         for (;;) {
             ++st_stages;
+            // lanes whose tt-ball is already inside the scanned region are done:
+            // they take no more entries, and the candidate filter (box, max tau)
+            // covers only the others (one sparse lane no longer drags 31 dense
+            // lanes' worth of candidates through every stage)
+            const bool open = active && !done;
+            float tau_s = open ? tau : -1.0f;
+#pragma unroll
+            for (int d = 0; d < DE; ++d) {
+                qlo[d] = DE <= kFilterDE ? tile::warp_min_f(open ? q[d] : kInf) : 0.0f;
+                qhi[d] = DE <= kFilterDE ? tile::warp_max_f(open ? q[d] : -kInf) : 0.0f;
+            }
             const Box<NL> cur = make_box<DB>(rho2, lo, hi, invw, nb, slack);
             for (int rb = 0; rb < cur.rows; rb += 32) {
                 const int rw = rb + lane;
@@ -707,13 +991,20 @@ __global__ void __maxnreg__(224) k_hd_search(const __grid_constant__ tile::TileA
                         }
                     }
                 }
-                scan_spans<NV, DE, X64>(W, a, S0, L0, qd, tau, tt, m, keep, q, qid, r, bd_base,
-                                        bp_base, st_chunks, st_cuts);
-                scan_spans<NV, DE, X64>(W, a, S1, L1, qd, tau, tt, m, keep, q, qid, r, bd_base,
-                                        bp_base, st_chunks, st_cuts);
+                scan_spans<NV, DE, X64>(W, a, S0, L0, qd, tau_s, tt, m, keep, q, qid, r, bd_base,
+                                        bp_base, qlo, qhi, t.boxes, ring, false, st_chunks, st_cuts);
+                scan_spans<NV, DE, X64>(W, a, S1, L1, qd, tau_s, tt, m, keep, q, qid, r, bd_base,
+                                        bp_base, qlo, qhi, t.boxes, ring, false, st_chunks, st_cuts);
             }
-            tighten();  // every lane to its keep-th smallest entry
-            const float need_t = tile::warp_max_f(active ? tt : 0.0f);
+            scan_spans<NV, DE, X64>(W, a, 0, 0, qd, tau_s, tt, m, keep, q, qid, r, bd_base, bp_base, qlo,
+                                    qhi, t.boxes, ring, true, st_chunks, st_cuts);  // flush the ring
+            if (open) tau = tau_s;
+            float need_t = tile::warp_max_f(open ? tt : 0.0f);
+            if (!(need_t <= rho2) && rho2 < diag2) {  // the bounds as they stand do not settle it
+                tighten();  // every open lane to its keep-th smallest entry
+                need_t = tile::warp_max_f(open ? tt : 0.0f);
+            }
+            done |= open && tt <= rho2;
             prev = cur;
             // done when every lane's tt-ball is inside the region, or the region
             // is the whole grid box of the split (lanes short of k-1 points)
@@ -785,6 +1076,9 @@ __global__ void __maxnreg__(224) k_hd_search(const __grid_constant__ tile::TileA
             }
         }
         __syncwarp();
+        if (a.stats && lane == 0)  // the slowest tile (clock64 cycles): the kernel's tail
+            atomicMax(a.stats + search::ST_COUNT + tile::TS_COUNT + HS_MAXCYC,
+                      (unsigned long long)(clock64() - tile_c0));
     }
     if (a.stats && lane == 0) {
         unsigned long long* hs = a.stats + search::ST_COUNT + tile::TS_COUNT;
@@ -905,6 +1199,24 @@ __global__ void __launch_bounds__(1024) k_dense_morton(const tile::TileArgs t) {
     }
 }
 
+// Bounding box of every 32 sorted positions of the search's coordinates (d <= 4).
+static __global__ void __launch_bounds__(256) k_block_boxes(const tile::TileArgs t) {
+    const int64_t b = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = lane_id();
+    if ((b << 5) >= t.n || tile::gated_off(t)) return;
+    const int64_t p = (b << 5) + lane;
+    const bool ok = p < t.n;
+    const float4 x = ok ? t.sc[p] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 lo = make_float4(tile::warp_min_f(ok ? x.x : kInf), tile::warp_min_f(ok ? x.y : kInf),
+                                  tile::warp_min_f(ok ? x.z : kInf), tile::warp_min_f(ok ? x.w : kInf));
+    const float4 hi = make_float4(tile::warp_max_f(ok ? x.x : -kInf), tile::warp_max_f(ok ? x.y : -kInf),
+                                  tile::warp_max_f(ok ? x.z : -kInf), tile::warp_max_f(ok ? x.w : -kInf));
+    if (lane == 0) {
+        t.boxes[2 * b] = lo;
+        t.boxes[2 * b + 1] = hi;
+    }
+}
+
 // Tile list, then the search (no redo: cuts fall back to exact keys).
 template <int NV, int DB, int DE, bool X64>
 int launch_hd(tile::TileArgs& t_in, const search::KnnArgs& a_in, cudaStream_t st) {
@@ -929,6 +1241,12 @@ int launch_hd(tile::TileArgs& t_in, const search::KnnArgs& a_in, cudaStream_t st
         t.sid = t.sid2;
         a.sc = t.sc2;
         a.sid = t.sid2;
+    }
+    if (DE <= kFilterDE && NV == 1 && t.boxes) {
+        k_block_boxes<<<(unsigned)ceil_div(t.n, 256), 256, 0, st>>>(t);
+        FG_TRY(launched(st));
+    } else {
+        t.boxes = nullptr;
     }
     constexpr size_t smem = hd_smem_bytes<DE>();
     auto kern = k_hd_search<NV, DB, DE, X64>;

@@ -99,6 +99,11 @@ struct TileArgs {
     float4* sc2;
     int32_t* sid2;
     int32_t* dense;
+    // hd path: points per tile (1..32; tiles[t] = (block, first point in block order))
+    uint8_t* tcnt;
+    // hd path, d <= 4: bounding box (lo, hi) of every 32 sorted positions of
+    // the search's coordinates (2 float4 per block; null: not used)
+    float4* boxes;
     // hd path as the clustered-data fallback of the d <= 4 tile path: run only
     // when *gate * 4 > n (the tile kernels declined the data); null: always
     const int* gate;

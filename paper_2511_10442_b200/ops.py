@@ -50,7 +50,7 @@ def set_debug_flags(flags: int) -> None:
 def knn_stats(reset: bool = True) -> dict:
     names = ("queries", "regions", "chunks", "appends", "compactions", "spec_fail", "exact_epi",
              "rows", "tiles", "tile_candidates", "tile_redo", "tile_fail", "tile_expanded",
-             "tile_evaluated", "hd_tiles", "hd_chunks", "hd_stages", "hd_redo", "hd_cuts")
+             "tile_evaluated", "hd_tiles", "hd_chunks", "hd_stages", "hd_max_tile_cycles", "hd_cuts")
     buf = (ctypes.c_uint64 * len(names))()
     _lib.check(_lib.load().fg_knn_stats(ctypes.cast(buf, ctypes.c_void_p), len(names), int(reset)))
     return dict(zip(names, [int(x) for x in buf]))
