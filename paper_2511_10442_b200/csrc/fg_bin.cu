@@ -17,6 +17,8 @@
 //                    compaction over the split) -- and every segment's
 //                    coordinates are gathered into sorted_coords with 16-byte
 //                    stores (float4 rows padded to 4*ceil(n_c/4)).
+#include <cooperative_groups.h>
+
 #include "fg_common.cuh"
 #include "fg_scan.cuh"
 
@@ -297,51 +299,67 @@ __global__ void __launch_bounds__(1024) k_fix_medium(const int32_t* __restrict__
 }
 
 // Huge cells: the members of cell c in ascending id order are exactly the
-// vertices v of its split with bin_idx[v] == c, so one CTA compacts the
-// split range in order (block-wide exclusive scan per chunk).
+// vertices v of its split with bin_idx[v] == c, in order.  A cluster of
+// kBigCtas CTAs takes one big cell: each CTA owns 1/kBigCtas of the split
+// range and each of its warps a contiguous slice of that; pass 1 counts the
+// slice's members (ballots, no block barriers), one block scan + a scan over
+// the cluster's CTAs through distributed shared memory give every warp its
+// output offset, pass 2 writes the members in order (ballot ranks) and
+// gathers their coordinates.  One CTA walking the whole split took 217 us at
+// config B (200k points, ~15 big cells).
+constexpr int kBigCtas = 8;
+constexpr int kBigThreads = 512;
+
 template <int NV, typename T>
-__global__ void __launch_bounds__(1024) k_fix_big(const int32_t* __restrict__ bounds,
-                                                  const int64_t* __restrict__ bin_idx,
-                                                  const int64_t* __restrict__ rs, int64_t total,
-                                                  int32_t* __restrict__ sort_order,
-                                                  const T* __restrict__ coords, int n_c,
-                                                  float4* __restrict__ sorted,
-                                                  const unsigned* __restrict__ counters,
-                                                  const int32_t* __restrict__ big) {
-    __shared__ int32_t s_warp[32];
-    __shared__ int32_t s_run;
+__global__ void __cluster_dims__(kBigCtas, 1, 1) __launch_bounds__(kBigThreads)
+k_fix_big(const int32_t* __restrict__ bounds, const int64_t* __restrict__ bin_idx,
+          const int64_t* __restrict__ rs, int64_t total, int32_t* __restrict__ sort_order,
+          const T* __restrict__ coords, int n_c, float4* __restrict__ sorted,
+          const unsigned* __restrict__ counters, const int32_t* __restrict__ big) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    constexpr int kW = kBigThreads / 32;
+    __shared__ int32_t s_warp[kW];
+    __shared__ int32_t s_cta;  // this CTA's member count (read by the cluster)
     const unsigned count = counters[2];
-    for (unsigned it = blockIdx.x; it < count; it += gridDim.x) {
+    const int rank = (int)cluster.block_rank();
+    const unsigned n_clusters = gridDim.x / kBigCtas;
+    const int w = threadIdx.x >> 5, lane = lane_id();
+    for (unsigned it = blockIdx.x / kBigCtas; it < count; it += n_clusters) {
         const int32_t c = big[it];
         const int64_t s = c / total;
         const int32_t lo = bounds[c];
         const int64_t v0 = rs[s], v1 = rs[s + 1];
-        if (threadIdx.x == 0) s_run = 0;
+        const int64_t per_cta = (v1 - v0 + kBigCtas - 1) / kBigCtas;
+        const int64_t a0 = v0 + per_cta * rank, a1 = min(v1, a0 + per_cta);
+        const int64_t per_w = (max(a1 - a0, (int64_t)0) + kW - 1) / kW;
+        const int64_t b0 = a0 + per_w * w, b1 = min(a1, b0 + per_w);
+        int cnt = 0;
+        for (int64_t v = b0 + lane; v - lane < b1; v += 32)
+            cnt += __popc(__ballot_sync(FG_FULL_MASK, v < b1 && bin_idx[v] == c));
+        if (lane == 0) s_warp[w] = cnt;
         __syncthreads();
-        for (int64_t b = v0; b < v1; b += blockDim.x) {
-            const int64_t v = b + threadIdx.x;
-            const int flag = (v < v1 && bin_idx[v] == c) ? 1 : 0;
-            const int w = threadIdx.x >> 5, lane = lane_id();
-            const int incl = warp_inclusive_scan(flag);
-            if (lane == 31) s_warp[w] = incl;
-            __syncthreads();
-            if (w == 0) {
-                int x = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0;
-                x = warp_inclusive_scan(x);
-                s_warp[lane] = x;
-            }
-            __syncthreads();
-            const int excl = incl - flag + (w > 0 ? s_warp[w - 1] : 0);
-            const int run = s_run;
-            if (flag) sort_order[lo + run + excl] = (int32_t)v;
-            __syncthreads();
-            if (threadIdx.x == 0) s_run = run + s_warp[(blockDim.x >> 5) - 1];
-            __syncthreads();
+        if (w == 0) {
+            const int x = lane < kW ? s_warp[lane] : 0;
+            const int incl = warp_inclusive_scan(x);
+            if (lane < kW) s_warp[lane] = incl - x;
+            if (lane == kW - 1) s_cta = incl;
         }
-        const int32_t len = bounds[c + 1] - lo;
-        for (int i = threadIdx.x; i < len; i += blockDim.x)
-            gather_row<NV>(coords, n_c, sort_order[lo + i], sorted + (int64_t)(lo + i) * NV);
-        __syncthreads();
+        cluster.sync();  // every CTA's count visible cluster-wide
+        int base = 0;
+        for (int r = 0; r < rank; ++r) base += *cluster.map_shared_rank(&s_cta, r);
+        int out = lo + base + s_warp[w];
+        for (int64_t v = b0 + lane; v - lane < b1; v += 32) {
+            const bool mem = v < b1 && bin_idx[v] == c;
+            const unsigned bal = __ballot_sync(FG_FULL_MASK, mem);
+            if (mem) {
+                const int p = out + __popc(bal & lanemask_lt());
+                sort_order[p] = (int32_t)v;
+                gather_row<NV>(coords, n_c, (int32_t)v, sorted + (int64_t)p * NV);
+            }
+            out += __popc(bal);
+        }
+        cluster.sync();  // s_cta / s_warp are reused by the next cell
     }
 }
 
@@ -358,8 +376,8 @@ int launch_fixups(const int32_t* bounds, int64_t n_cells, int32_t* sort_order, c
     k_fix_medium<NV, T><<<296, 1024, 0, st>>>(bounds, sort_order, coords, n_c, s4, w.counters,
                                            w.medium);
     FG_TRY(launched(st));
-    k_fix_big<NV, T><<<148, 1024, 0, st>>>(bounds, bin_idx, rs, total, sort_order, coords, n_c, s4,
-                                        w.counters, w.big);
+    k_fix_big<NV, T><<<kBigCtas * 37, kBigThreads, 0, st>>>(bounds, bin_idx, rs, total, sort_order,
+                                                             coords, n_c, s4, w.counters, w.big);
     return launched(st);
 }
 

@@ -123,6 +123,20 @@ def test_bin_empty_splits_and_huge_cells(oracle):
         assert np.array_equal(r, g_.astype(r.dtype))
 
 
+def test_bin_clustered_config_b_vs_oracle(oracle):
+    """Config B (200k clustered points): many medium and big cells (the
+    cluster-parallel big-cell fix-up) -- bin arrays equal to the oracle's."""
+    from paper_2511_10442_b200.datasets import config_dataset
+    c, off, k = config_dataset("B")
+    nb = fg.compute_n_bins(int(np.diff(off).max()), k, 4)
+    ref = oracle.build_index(c.astype(np.float64), off, 4, nb)
+    got = run_bin(c, off, 4, nb)
+    for r, g_ in zip(ref, got[:5]):
+        assert np.array_equal(r, g_.astype(r.dtype))
+    n_c = c.shape[1]
+    assert np.array_equal(got[5][:, :n_c], c[ref[1]])
+
+
 def test_bin_fp64_cell_kat():
     # SURVEY App. B: generate_dataset(1_000_000, 4, seed=1) as f32, vertex 842094,
     # dim 3: float64 cell arithmetic gives 28 (float32 would give 27).
