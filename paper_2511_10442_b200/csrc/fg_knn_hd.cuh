@@ -44,7 +44,10 @@
 namespace fg {
 namespace hd {
 
-constexpr int kWarps = 2;      // warps per CTA
+#ifndef FG_HD_WARPS
+#define FG_HD_WARPS 2
+#endif
+constexpr int kWarps = FG_HD_WARPS;  // warps per CTA
 #ifndef FG_HD_UNROLL
 #define FG_HD_UNROLL 4
 #endif
