@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(1024) k_fix_medium(const int32_t* __restrict__
         for (int size = 2; size <= p2; size <<= 1)
             for (int stride = size >> 1; stride > 0; stride >>= 1) {
                 for (int i = threadIdx.x; i < p2 / 2; i += blockDim.x) {
-                    const int a = 2 * stride * (i / stride) + (i % stride), b = a + stride;
+                    const int a = ((i & ~(stride - 1)) << 1) | (i & (stride - 1)), b = a + stride;  // stride: a power of 2
                     const bool up = (a & size) == 0;
                     const int32_t x = s[a], y = s[b];
                     if ((x > y) == up) {

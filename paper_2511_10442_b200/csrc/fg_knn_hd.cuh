@@ -1182,7 +1182,7 @@ __global__ void __launch_bounds__(1024) k_dense_morton(const tile::TileArgs t) {
         for (int size = 2; size <= p2; size <<= 1)
             for (int stride = size >> 1; stride > 0; stride >>= 1) {
                 for (int i = threadIdx.x; i < p2 / 2; i += blockDim.x) {
-                    const int x0 = 2 * stride * (i / stride) + (i % stride), x1 = x0 + stride;
+                    const int x0 = ((i & ~(stride - 1)) << 1) | (i & (stride - 1)), x1 = x0 + stride;  // stride: a power of 2
                     const bool up = (x0 & size) == 0;
                     const unsigned long long ka = key[x0], kb = key[x1];
                     if ((ka > kb) == up) {
