@@ -153,11 +153,7 @@ __global__ void __launch_bounds__(128) k_hd_tiles(const tile::TileArgs a) {
                 emit(g0, run);
                 run = 0;
             }
-            while (cnt > 0) {
-                if (run == 0) {
-                    c0 = c;
-                    g0 = g;
-                }
+            if (run > 0) {  // top up the open run
                 const int take = min(cnt, 32 - run);
                 run += take;
                 cnt -= take;
@@ -166,6 +162,23 @@ __global__ void __launch_bounds__(128) k_hd_tiles(const tile::TileArgs a) {
                     emit(g0, run);
                     run = 0;
                 }
+            }
+            if (cnt >= 32) {  // whole runs of this column, written in parallel
+                const int nf = cnt >> 5;
+                if (pass == 1)
+                    for (int i = lane; i < nf; i += 32) {
+                        a.tiles[t0 + nt + i] = make_int2(blk, g + 32 * i);
+                        a.tcnt[t0 + nt + i] = (uint8_t)32;
+                    }
+                nt += nf;
+                g += 32 * nf;
+                cnt -= 32 * nf;
+            }
+            if (cnt > 0) {  // a new open run
+                c0 = c;
+                g0 = g;
+                run = cnt;
+                g += cnt;
             }
         }
         if (run > 0) emit(g0, run);
