@@ -114,6 +114,9 @@ struct TileWs {
     int32_t* dense;
     float4* boxes;   // hd path, d <= 4: per-32-position bounding boxes
     uint8_t* tcnt;   // hd path: points per tile
+    uint8_t* tkey;   //          cost bucket per tile
+    int* hist;       //          bucket counts / cursors
+    int32_t* order;  //          dispatch order
     int32_t* lists;  // split epilogue: n * kCap sorted positions
     float2* meta;    //                 n * (tau, m)
     size_t bytes;
@@ -170,6 +173,12 @@ TileWs hd_ws(void* base, int64_t n, int32_t n_coords, int32_t n_splits, int32_t 
     off = align_up(off + sizeof(int32_t) * (size_t)(n / (hd::kDenseCell + 1) + 1), 256);
     w.tcnt = reinterpret_cast<uint8_t*>(p + off);
     off = align_up(off + (size_t)max_tiles, 256);
+    w.tkey = reinterpret_cast<uint8_t*>(p + off);
+    off = align_up(off + (size_t)max_tiles, 256);
+    w.hist = reinterpret_cast<int*>(p + off);
+    off = align_up(off + sizeof(int) * 2 * hd::kCostBuckets, 256);
+    w.order = reinterpret_cast<int32_t*>(p + off);
+    off = align_up(off + sizeof(int32_t) * (size_t)max_tiles, 256);
     w.boxes = nullptr;
     if (n_coords <= hd::kFilterDE) {
         w.boxes = reinterpret_cast<float4*>(p + off);
@@ -308,6 +317,9 @@ extern "C" int fg_knn_fwd_ws(const float* sorted_coords, const int32_t* sort_ord
         th.dense = wh.dense;
         th.boxes = wh.boxes;
         th.tcnt = wh.tcnt;
+        th.tkey = wh.tkey;
+        th.hist = wh.hist;
+        th.order = wh.order;
         th.stats = nullptr;
         int* hint_dev = nullptr;
         bool last_clustered = true;
@@ -343,6 +355,9 @@ extern "C" int fg_knn_fwd_ws(const float* sorted_coords, const int32_t* sort_ord
         t.dense = w.dense;
         t.boxes = w.boxes;
         t.tcnt = w.tcnt;
+        t.tkey = w.tkey;
+        t.hist = w.hist;
+        t.order = w.order;
         switch ((n_coords + 3) / 4) {
             case 1: return hd::dispatch_hd_nv1(t, a, d_bin, st);
             case 2: return hd::dispatch_hd_nv2(t, a, d_bin, st);
@@ -445,6 +460,9 @@ extern "C" int fg_knn_fwd_f64_ws(const double* coords, const float* sorted_coord
     t.dense = w.dense;
     t.boxes = w.boxes;
     t.tcnt = w.tcnt;
+    t.tkey = w.tkey;
+    t.hist = w.hist;
+    t.order = w.order;
     switch ((n_coords + 3) / 4) {
         case 1: return hd::dispatch_hd_nv1(t, a, d_bin, st);
         case 2: return hd::dispatch_hd_nv2(t, a, d_bin, st);

@@ -189,6 +189,114 @@ __global__ void __launch_bounds__(128) k_hd_tiles(const tile::TileArgs a) {
     }
 }
 
+// Lane -> sorted position of tile ti's point `lane` (-1: none): the block's
+// points in (column, row) order, lanes [0, tcnt) from the tile's start.
+template <int DB>
+__device__ __forceinline__ int32_t tile_point(const tile::TileArgs& t, int ti) {
+    constexpr int NL = DB - 1;
+    const int lane = lane_id();
+    const int2 td = t.tiles[ti];
+    const int blk = td.x, start = td.y, tlen = t.tcnt[ti];
+    const int s = blk / t.bps;
+    int o[NL > 0 ? NL : 1];
+    tile::block_origin<NL>(blk - s * t.bps, t.nblk, o);
+    const int64_t cbase = (int64_t)s * t.total;
+    const int nb = t.nb;
+    int col = 0;
+    if (lane < nb) {
+#pragma unroll
+        for (int rr = 0; rr < (1 << NL); ++rr) {
+            int rowflat = 0;
+            bool ok = true;
+#pragma unroll
+            for (int i = 0; i < NL; ++i) {
+                const int j = o[i] + ((rr >> (NL - 1 - i)) & 1);
+                ok &= j < nb;
+                rowflat = rowflat * nb + j;
+            }
+            if (ok) {
+                const int64_t rc = cbase + (int64_t)rowflat * nb + lane;
+                col += t.bounds[rc + 1] - t.bounds[rc];
+            }
+        }
+    }
+    const int P = warp_inclusive_scan(col);
+    const int g = start + lane;
+    int c = 0;
+    for (int cc = 0; cc < nb; ++cc) c += __shfl_sync(FG_FULL_MASK, P, cc) <= g ? 1 : 0;
+    const int Ptot = __shfl_sync(FG_FULL_MASK, P, 31);
+    const int Pprev = __shfl_sync(FG_FULL_MASK, P, max(c - 1, 0));
+    int32_t p = -1;
+    if (lane < tlen && g < Ptot && c < nb) {
+        int off = g - (c > 0 ? Pprev : 0);
+        for (int rr = 0; rr < (1 << NL); ++rr) {
+            int rowflat = 0;
+            bool ok = true;
+#pragma unroll
+            for (int i = 0; i < NL; ++i) {
+                const int j = o[i] + ((rr >> (NL - 1 - i)) & 1);
+                ok &= j < nb;
+                rowflat = rowflat * nb + j;
+            }
+            if (!ok) continue;
+            const int64_t rc = cbase + (int64_t)rowflat * nb + c;
+            const int32_t b0 = t.bounds[rc], len = t.bounds[rc + 1] - b0;
+            if (off < len) {
+                p = b0 + off;
+                break;
+            }
+            off -= len;
+        }
+    }
+    return p;
+}
+
+// Dispatch order: a tile's cost grows with its query box (a wide box reaches
+// far more candidates), and a costly tile taken last is the kernel's tail
+// (config B: one tile took half the kernel's time).  Tiles are counted into
+// 64 buckets of log2(box diagonal^2) (k_hd_cost), the buckets laid out widest
+// first (k_hd_rank) and the tiles placed (k_hd_place); the search takes them in
+// that order.
+constexpr int kCostBuckets = 64;
+
+template <int NV, int DB>
+__global__ void __launch_bounds__(128) k_hd_cost(const tile::TileArgs t) {
+    const int ti = blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (ti >= t.ctr[0] || tile::gated_off(t)) return;
+    const int32_t p = tile_point<DB>(t, ti);
+    const bool live = p >= 0;
+    const float4 x = live ? t.sc[(int64_t)p * NV] : make_float4(0.f, 0.f, 0.f, 0.f);
+    float d2 = 0.0f;
+    const float xa[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+        const float e = tile::warp_max_f(live ? xa[d] : -kInf) - tile::warp_min_f(live ? xa[d] : kInf);
+        d2 = fmaf(e, e, d2);
+    }
+    if (lane_id() == 0) {
+        int b = 0;  // bucket 0: the widest boxes
+        if (d2 > 0.0f && d2 < kInf) b = min(max(40 - ilogbf(d2), 0), kCostBuckets - 1);
+        if (!(d2 < kInf)) b = 0;
+        t.tkey[ti] = (uint8_t)b;
+        atomicAdd(&t.hist[b], 1);
+    }
+}
+
+static __global__ void k_hd_rank(const tile::TileArgs t) {
+    if (tile::gated_off(t)) return;
+    const int lane = threadIdx.x;  // one warp: 64 buckets, 2 per lane
+    const int a0 = t.hist[2 * lane], a1 = t.hist[2 * lane + 1];
+    const int incl = warp_inclusive_scan(a0 + a1);
+    t.hist[kCostBuckets + 2 * lane] = incl - a0 - a1;
+    t.hist[kCostBuckets + 2 * lane + 1] = incl - a1;
+}
+
+static __global__ void __launch_bounds__(256) k_hd_place(const tile::TileArgs t) {
+    const int ti = blockIdx.x * blockDim.x + threadIdx.x;
+    if (ti >= t.ctr[0] || tile::gated_off(t)) return;
+    t.order[atomicAdd(&t.hist[kCostBuckets + t.tkey[ti]], 1)] = ti;
+}
+
 // ---------------------------------------------------------------- helpers
 __device__ __forceinline__ unsigned long long dup2(float x) {
     unsigned long long r;
@@ -812,62 +920,14 @@ __global__ void __maxnreg__(224) k_hd_search(const __grid_constant__ tile::TileA
         if (lane == 0) ti = atomicAdd(&t.ctr[1], 1);
         ti = __shfl_sync(FG_FULL_MASK, ti, 0);
         if (ti >= n_tiles) break;
+        if (t.order) ti = t.order[ti];
         ++st_tiles;
         const long long tile_c0 = clock64();
-        const int2 td = t.tiles[ti];
-        const int blk = td.x, start = td.y, tlen = t.tcnt[ti];
-        const int s = blk / t.bps;
-        int o[NL > 0 ? NL : 1];
-        tile::block_origin<NL>(blk - s * t.bps, t.nblk, o);
+        const int s = t.tiles[ti].x / t.bps;
         const int64_t cbase = (int64_t)s * t.total;
 
-        // ---- lane -> point (start + lane) of the block in (column, row) order
-        int col = 0;
-        if (lane < nb) {
-#pragma unroll
-            for (int rr = 0; rr < (1 << NL); ++rr) {
-                int rowflat = 0;
-                bool ok = true;
-#pragma unroll
-                for (int i = 0; i < NL; ++i) {
-                    const int j = o[i] + ((rr >> (NL - 1 - i)) & 1);
-                    ok &= j < nb;
-                    rowflat = rowflat * nb + j;
-                }
-                if (ok) {
-                    const int64_t rc = cbase + (int64_t)rowflat * nb + lane;
-                    col += t.bounds[rc + 1] - t.bounds[rc];
-                }
-            }
-        }
-        const int P = warp_inclusive_scan(col);
-        const int g = start + lane;
-        int c = 0;
-        for (int cc = 0; cc < nb; ++cc) c += __shfl_sync(FG_FULL_MASK, P, cc) <= g ? 1 : 0;
-        const int Ptot = __shfl_sync(FG_FULL_MASK, P, 31);
-        const int Pprev = __shfl_sync(FG_FULL_MASK, P, max(c - 1, 0));
-        int32_t p = -1;
-        if (lane < tlen && g < Ptot && c < nb) {
-            int off = g - (c > 0 ? Pprev : 0);
-            for (int rr = 0; rr < (1 << NL); ++rr) {
-                int rowflat = 0;
-                bool ok = true;
-#pragma unroll
-                for (int i = 0; i < NL; ++i) {
-                    const int j = o[i] + ((rr >> (NL - 1 - i)) & 1);
-                    ok &= j < nb;
-                    rowflat = rowflat * nb + j;
-                }
-                if (!ok) continue;
-                const int64_t rc = cbase + (int64_t)rowflat * nb + c;
-                const int32_t b0 = t.bounds[rc], len = t.bounds[rc + 1] - b0;
-                if (off < len) {
-                    p = b0 + off;
-                    break;
-                }
-                off -= len;
-            }
-        }
+        // ---- lane -> point of the tile
+        const int32_t p = tile_point<DB>(t, ti);
         const bool live = p >= 0;
         if (!__any_sync(FG_FULL_MASK, live)) continue;
         const int32_t qid = live ? a.sid[p] : 0;
@@ -1263,6 +1323,20 @@ int launch_hd(tile::TileArgs& t_in, const search::KnnArgs& a_in, cudaStream_t st
         FG_TRY(launched(st));
     } else {
         t.boxes = nullptr;
+    }
+#ifndef FG_HD_ORDER
+#define FG_HD_ORDER 1
+#endif
+    if (!FG_HD_ORDER) t.order = nullptr;
+    if (t.order) {  // widest query boxes first
+        const int64_t max_tiles = t.n / 32 + (int64_t)t.n_blocks * t.nb + 1;  // hd_ws's bound
+        FG_CUDA(cudaMemsetAsync(t.hist, 0, sizeof(int) * 2 * kCostBuckets, st));
+        k_hd_cost<NV, DB><<<(unsigned)ceil_div(max_tiles, 4), 128, 0, st>>>(t);
+        FG_TRY(launched(st));
+        k_hd_rank<<<1, 32, 0, st>>>(t);
+        FG_TRY(launched(st));
+        k_hd_place<<<(unsigned)ceil_div(max_tiles, 256), 256, 0, st>>>(t);
+        FG_TRY(launched(st));
     }
     constexpr size_t smem = hd_smem_bytes<DE>();
     auto kern = k_hd_search<NV, DB, DE, X64>;

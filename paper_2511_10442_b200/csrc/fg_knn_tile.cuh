@@ -101,6 +101,11 @@ struct TileArgs {
     int32_t* dense;
     // hd path: points per tile (1..32; tiles[t] = (block, first point in block order))
     uint8_t* tcnt;
+    // hd path dispatch order (widest query boxes first): per-tile cost bucket,
+    // bucket counts / cursors (2 x 64), the order (null: tile order)
+    uint8_t* tkey;
+    int* hist;
+    int32_t* order;
     // hd path, d <= 4: bounding box (lo, hi) of every 32 sorted positions of
     // the search's coordinates (2 float4 per block; null: not used)
     float4* boxes;
