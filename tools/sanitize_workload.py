@@ -54,6 +54,19 @@ def hd_cases():
     bi, so, bb, mins, widths, sc = ops.bin_by_coordinates(c64, rs, 5, nb)
     ops.binned_select_knn(c64, rs, bi, so, bb, mins, widths, sc, 16, 5, nb, None, 0.05, False, True)
     ops.binned_select_knn(c64, rs, bi, so, bb, mins, widths, sc, 100, 5, nb, None, None, False, True)
+    # clustered d <= 4: the gated fallback (dense cells in Morton order, block
+    # boxes, cost-ordered dispatch); the second call launches it (device hint)
+    xc, _ = generate_dataset(12000, 4, splits=1, seed=2, distribution="clusters")
+    for _ in range(2):
+        run(xc, np.array([0, 12000], np.int64), 40, 4)
+    xc3, _ = generate_dataset(6000, 3, splits=2, seed=3, distribution="clusters")
+    for _ in range(2):
+        run(xc3, np.array([0, 2500, 6000], np.int64), 12, 3)
+    # d = 4 with d_bin = 2: the hd path with the candidate filter
+    run(x6[:, :4].copy(), off6, 16, 2)
+    # binning with a big cell (> 4096 points: the cluster fix-up)
+    xb = np.concatenate([np.full((5000, 3), 0.25), rng.random((3000, 3))])
+    run(xb, np.array([0, 8000], np.int64), 8, 3)
     torch.cuda.synchronize()
 
 
