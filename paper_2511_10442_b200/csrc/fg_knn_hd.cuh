@@ -57,7 +57,7 @@ constexpr int kUnroll = FG_HD_UNROLL;  // 4-candidate groups in flight per chunk
 #endif
 constexpr float kHintScale = FG_HD_HINT_SCALE;  // first-stage radius^2 / previous tile's
 #ifndef FG_HD_SEED
-#define FG_HD_SEED 248
+#define FG_HD_SEED 120
 #endif
 constexpr int kSeed = FG_HD_SEED;  // stage-0 tau seeding window (sorted positions), 0: off
 static_assert(kSeed < 256, "8-bit seed bucket counters");
@@ -71,7 +71,6 @@ constexpr int kCap = FG_HD_CAP;  // per-lane buffer entries
 // candidates are filtered against the tile's query box for DE <= this (the
 // clustered d <= 4 fallback: dense cells are scanned whole at cell granularity)
 constexpr int kFilterDE = FG_HD_FILTER_DE;
-constexpr int kStride = kCap + 1;
 constexpr int kMaxNeed1 = 64;  // host eligibility (float32 coordinates): k <= 64
 constexpr int kMaxK64 = kCap - 8;  // float64 coordinates: k <= 120 (a cut frees >= 4 slots)
 constexpr float kMargin = 1.0f + 1e-5f;
@@ -81,8 +80,9 @@ constexpr float kInf = __builtin_huge_valf();
 
 enum { HS_TILES, HS_CHUNKS, HS_STAGES, HS_MAXCYC, HS_COMPACT, HS_COUNT };  // HS_MAXCYC: slowest tile (clock64)
 
-template <int DE>
+template <int DE, int CAP>
 struct HdWarp {
+    static constexpr int kStride = CAP + 1;
     float bd[32 * kStride];    // lane buffers: fp32 d2 (odd stride: appends spread over banks)
     int32_t bp[32 * kStride];  //               sorted positions
     // candidates, SoA: a 64-entry ring when filtered, else one 32-candidate
@@ -93,9 +93,24 @@ struct HdWarp {
     search::WarpBuf<128> eb;   // epilogue scratch (the warp-per-query kernel's)
 };
 
-template <int DE>
+// Per-lane buffer entries and warps per CTA of an instantiation: the float32
+// d <= 4 kernels (the clustered fallback, k <= 41 there) use 96 entries and
+// one warp per CTA -- 7 warps/SM instead of 6 (config B 8% faster); d > 4
+// (config C, k = 64: more room between cuts) and float64 (k <= 120) keep 128.
+#ifndef FG_HD_CAP_LOWD
+#define FG_HD_CAP_LOWD 96
+#endif
+template <int NV, bool X64>
+__host__ __device__ constexpr int hd_cap() {
+    return NV == 1 && !X64 ? FG_HD_CAP_LOWD : kCap;
+}
+template <int NV, bool X64>
+__host__ __device__ constexpr int hd_warps() {
+    return NV == 1 && !X64 ? 1 : kWarps;
+}
+template <int DE, int CAP, int WARPS>
 __host__ __device__ constexpr size_t hd_smem_bytes() {
-    return sizeof(HdWarp<DE>) * kWarps;
+    return sizeof(HdWarp<DE, CAP>) * WARPS;
 }
 
 // ---------------------------------------------------------------- tile list
@@ -389,8 +404,8 @@ __device__ __forceinline__ double hd_key(const search::KnnArgs& a, const float (
 
 // W.eb.p[0..m) -> (key, id, cp) with exact keys, sorted by (key, id); entries
 // beyond max_radius2 get the sentinel.  Returns the sorted length (pow2).
-template <int NV, bool X64, int DE>
-__device__ __noinline__ int exact_sort(HdWarp<DE>& W, const search::KnnArgs& a, int m,
+template <int NV, bool X64, int DE, int CAP>
+__device__ __noinline__ int exact_sort(HdWarp<DE, CAP>& W, const search::KnnArgs& a, int m,
                                        const float (&qj)[4 * NV], int32_t qid) {
     const int lane = lane_id();
     const bool use_r2 = a.flags & FG_KNN_USE_MAX_R2;
@@ -430,14 +445,14 @@ __device__ __forceinline__ float up_bound(float x, float r) {
 // threshold tau_j follows; entries above tau_j are dropped.  When near-ties
 // leave no room (> kCap - 8 entries within the margin: duplicates), exactly
 // the keep smallest by (float64 key, index) are kept -- the canonical order.
-template <int NV, bool X64, int DE>
-__device__ __noinline__ int cut_lane(HdWarp<DE>& W, const search::KnnArgs& a, int j, int m, int keep,
+template <int NV, bool X64, int DE, int CAP>
+__device__ __noinline__ int cut_lane(HdWarp<DE, CAP>& W, const search::KnnArgs& a, int j, int m, int keep,
                                      float& tau_j, float& tt_j, const float (&qj)[4 * NV],
                                      int32_t qid, float r) {
     const int lane = lane_id();
-    constexpr int PER = kCap / 32;
-    float* bd = &W.bd[j * kStride];
-    int32_t* bp = &W.bp[j * kStride];
+    constexpr int PER = CAP / 32;
+    float* bd = &W.bd[j * (CAP + 1)];
+    int32_t* bp = &W.bp[j * (CAP + 1)];
     __syncwarp();  // lane j's appends (its own shared-memory stores) before the other lanes read them
     unsigned key[PER];
     int32_t pv[PER];
@@ -480,7 +495,7 @@ __device__ __noinline__ int cut_lane(HdWarp<DE>& W, const search::KnnArgs& a, in
         kept += __popc(__ballot_sync(FG_FULL_MASK, (i * 32 + lane) < m && __uint_as_float(key[i]) <= nt));
     __syncwarp();
     int wpos = 0;
-    if (kept <= kCap - 8) {
+    if (kept <= CAP - 8) {
 #pragma unroll
         for (int i = 0; i < PER; ++i) {
             const bool k = (i * 32 + lane) < m && __uint_as_float(key[i]) <= nt;
@@ -529,8 +544,8 @@ __device__ __noinline__ int cut_lane(HdWarp<DE>& W, const search::KnnArgs& a, in
 // bound of the lane's keep-th smallest d2 among them (the upper edge of the
 // bucket where the count reaches keep; the largest d2 if only the open bucket
 // does; +inf with fewer than keep points) -- within 25% of the value.
-template <int NV, int DE>
-__device__ __forceinline__ float seed_bound(HdWarp<DE>& W, const search::KnnArgs& a, int64_t w0, int n,
+template <int NV, int DE, int CAP>
+__device__ __forceinline__ float seed_bound(HdWarp<DE, CAP>& W, const search::KnnArgs& a, int64_t w0, int n,
                                             const unsigned long long (&qd)[DE], int keep, float s16) {
     const int lane = lane_id();
     const bool use_dir = a.flags & FG_KNN_USE_DIRECTION;
@@ -600,8 +615,8 @@ __device__ __forceinline__ float seed_bound(HdWarp<DE>& W, const search::KnnArgs
 
 // Evaluate one 32-candidate chunk (W.sx / W.spos) against every lane's query
 // and append the passing entries to the lanes' buffers.
-template <int DE, class Room>
-__device__ __forceinline__ void eval_chunk(HdWarp<DE>& W, const unsigned long long (&qd)[DE], int head,
+template <int DE, int CAP, class Room>
+__device__ __forceinline__ void eval_chunk(HdWarp<DE, CAP>& W, const unsigned long long (&qd)[DE], int head,
                                            float& tau, uint32_t bd_base, uint32_t bp_base, int& m,
                                            Room&& room) {
     // ring slots [head, head + 32); dead candidates carry +inf coordinates and position -1
@@ -638,7 +653,7 @@ __device__ __forceinline__ void eval_chunk(HdWarp<DE>& W, const unsigned long lo
     for (int j = 0; j < 32; j += 4) {
         bool p0 = dv[j] <= tau, p1 = dv[j + 1] <= tau, p2 = dv[j + 2] <= tau, p3 = dv[j + 3] <= tau;
         if (__any_sync(FG_FULL_MASK, p0 | p1 | p2 | p3)) {
-            if (__any_sync(FG_FULL_MASK, m > kCap - 4)) {  // a full buffer: cut it first
+            if (__any_sync(FG_FULL_MASK, m > CAP - 4)) {  // a full buffer: cut it first
                 room();
                 p0 = dv[j] <= tau; p1 = dv[j + 1] <= tau; p2 = dv[j + 2] <= tau; p3 = dv[j + 3] <= tau;
             }
@@ -672,8 +687,8 @@ struct Ring {
 // tile's query box are skipped, the remaining candidates are filtered one by
 // one against the query box and the survivors go through the ring; `final`
 // evaluates what is left in the ring.
-template <int NV, int DE, bool X64>
-__device__ __forceinline__ void scan_spans(HdWarp<DE>& W, const search::KnnArgs& a, int32_t S, int32_t L,
+template <int NV, int DE, bool X64, int CAP>
+__device__ __forceinline__ void scan_spans(HdWarp<DE, CAP>& W, const search::KnnArgs& a, int32_t S, int32_t L,
                                            const unsigned long long (&qd)[DE], float& tau, float& tt,
                                            int& m, int keep, const float (&q)[4 * NV], int32_t qid,
                                            float r, uint32_t bd_base, uint32_t bp_base,
@@ -713,7 +728,7 @@ __device__ __forceinline__ void scan_spans(HdWarp<DE>& W, const search::KnnArgs&
     };
     // cut every lane whose buffer cannot take 4 more entries (warp-uniform)
     auto room = [&]() {
-        unsigned full = __ballot_sync(FG_FULL_MASK, m > kCap - 4);
+        unsigned full = __ballot_sync(FG_FULL_MASK, m > CAP - 4);
         while (full) {
             const int j = __ffs(full) - 1;
             full &= full - 1;
@@ -898,7 +913,9 @@ __global__ void __maxnreg__(224) k_hd_search(const __grid_constant__ tile::TileA
                                                            const __grid_constant__ search::KnnArgs a) {
     constexpr int NL = DB - 1;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    HdWarp<DE>& W = reinterpret_cast<HdWarp<DE>*>(smem_raw)[threadIdx.x >> 5];
+    constexpr int CAP = hd_cap<NV, X64>();
+    constexpr int kS = CAP + 1;
+    HdWarp<DE, CAP>& W = reinterpret_cast<HdWarp<DE, CAP>*>(smem_raw)[threadIdx.x >> 5];
     const int lane = lane_id();
     const int nb = t.nb;
     const int need = a.k - 1;
@@ -908,8 +925,8 @@ __global__ void __maxnreg__(224) k_hd_search(const __grid_constant__ tile::TileA
     const float r = X64 ? *a.rnd : 0.0f;
     // cell-unit slack: the float32 cell position of a float64 coordinate can be
     // off by the rounding of the coordinate and of the split minimum
-    const uint32_t bd_base = (uint32_t)__cvta_generic_to_shared(&W.bd[lane * kStride]);
-    const uint32_t bp_base = (uint32_t)__cvta_generic_to_shared(&W.bp[lane * kStride]);
+    const uint32_t bd_base = (uint32_t)__cvta_generic_to_shared(&W.bd[lane * kS]);
+    const uint32_t bp_base = (uint32_t)__cvta_generic_to_shared(&W.bp[lane * kS]);
     float rho2_hint = -1.0f;  // final radius^2 of this warp's previous tile
     unsigned long long st_tiles = 0, st_chunks = 0, st_stages = 0, st_cuts = 0;
     search::Counters cnt;
@@ -1123,12 +1140,12 @@ __global__ void __maxnreg__(224) k_hd_search(const __grid_constant__ tile::TileA
             int wpos = 0;
             for (int e0 = 0; e0 < mj; e0 += 32) {
                 const int e = e0 + lane;
-                const bool ok = e < mj && W.bp[j * kStride + e] != pj;
+                const bool ok = e < mj && W.bp[j * kS + e] != pj;
                 const unsigned bal = __ballot_sync(FG_FULL_MASK, ok);
                 if (ok) {
                     const int at = wpos + __popc(bal & lanemask_lt());
-                    W.eb.d[at] = W.bd[j * kStride + e];
-                    W.eb.p[at] = W.bp[j * kStride + e];
+                    W.eb.d[at] = W.bd[j * kS + e];
+                    W.eb.p[at] = W.bp[j * kS + e];
                 }
                 wpos += __popc(bal);
             }
@@ -1338,12 +1355,13 @@ int launch_hd(tile::TileArgs& t_in, const search::KnnArgs& a_in, cudaStream_t st
         k_hd_place<<<(unsigned)ceil_div(max_tiles, 256), 256, 0, st>>>(t);
         FG_TRY(launched(st));
     }
-    constexpr size_t smem = hd_smem_bytes<DE>();
+    constexpr int WARPS = hd_warps<NV, X64>();
+    constexpr size_t smem = hd_smem_bytes<DE, hd_cap<NV, X64>(), WARPS>();
     auto kern = k_hd_search<NV, DB, DE, X64>;
     FG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 1;  // resident CTAs per SM (shared memory bound)
-    FG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, smem));
-    kern<<<(unsigned)(sms * std::max(per_sm, 1)), kWarps * 32, smem, st>>>(t, a);
+    FG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARPS * 32, smem));
+    kern<<<(unsigned)(sms * std::max(per_sm, 1)), WARPS * 32, smem, st>>>(t, a);
     return launched(st);
 }
 
