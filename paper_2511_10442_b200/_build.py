@@ -50,15 +50,22 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
     tmp = os.path.join(PKG, "build" if not defines else "build_" + "_".join(d.replace("=", "") for d in defines))
     os.makedirs(tmp, exist_ok=True)
     procs = []
+    hdrs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
+    hdrs.append(os.path.join(ROOT, "include", "fastgraph_b200.h"))
+    t_hdr = max(os.path.getmtime(h) for h in hdrs)
     for src in sources():
         obj = os.path.join(tmp, os.path.basename(src).replace(".cu", ".o"))
+        objs.append(obj)
+        # incremental (not force): an object newer than its source and every header is reused
+        if (not force and os.path.exists(obj)
+                and os.path.getmtime(obj) > max(os.path.getmtime(src), t_hdr)):
+            continue
         cmd = [nvcc(), ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                *(["-Xptxas", "-v"] if verbose else []),
                *["-D" + d for d in defines],
                "-I" + os.path.join(ROOT, "include"), "-c", src, "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
                                             text=True)))
-        objs.append(obj)
     failed = False
     for src, p in procs:
         out, _ = p.communicate()

@@ -5,18 +5,21 @@
 //                    uint atomicMin/Max per block and dim.
 // K1b k_bbox_final   dim_mins / widths exactly as pyx:114-118 (float64).
 // K2 k_assign        cell = floor((x - min) / w) in float64, clamped, row-major
-//                    flat, global id; warp-aggregated (match_any) histogram.
+//                    flat, global id; warp-aggregated (match_any) histogram
+//                    whose returning atomics give every vertex a rank in its
+//                    cell (arrival order).
 // K3 k_scan          single-pass decoupled-look-back exclusive scan of the
 //                    histogram -> bin_bounds (+ a cursor copy).  CUB-free.
-// K4 k_scatter       atomic-cursor scatter into sort_order (warp-aggregated,
-//                    warp-local order kept), then the stable fix-up that makes
+// K4 k_place         vertex v goes to bin_bounds[cell] + rank (no second
+//                    atomic pass), its coordinates read coalesced and stored
+//                    to sorted_coords with 16-byte stores (float4 rows padded
+//                    to 4*ceil(n_c/4)); then the stable fix-up that makes
 //                    sort_order identical to the reference's stable counting
-//                    sort: each cell segment is re-sorted by vertex id --
-//                    k_fix_small (thread per cell, <= 32), k_fix_medium (CTA
-//                    bitonic in smem, <= 4096) and k_fix_big (CTA in-order
-//                    compaction over the split) -- and every segment's
-//                    coordinates are gathered into sorted_coords with 16-byte
-//                    stores (float4 rows padded to 4*ceil(n_c/4)).
+//                    sort: each cell segment is put in vertex-id order --
+//                    k_fix_small (thread per cell, <= 32: only segments the
+//                    arrival order left unsorted are rewritten), k_fix_medium
+//                    (CTA bitonic in smem, <= 4096) and k_fix_big (cluster
+//                    in-order compaction over the split) -- and re-gathered.
 #include <cooperative_groups.h>
 
 #include "fg_common.cuh"
@@ -39,6 +42,7 @@ struct BinWs {
     unsigned* counters;      // [0] scan tile ticket, [1] medium count, [2] big count
     int32_t* medium;         // medium cell list
     int32_t* big;            // big cell list
+    int32_t* rank;           // n: arrival rank of every vertex in its cell
     int64_t n_tiles;
     int64_t list_cap;
 };
@@ -60,6 +64,7 @@ size_t carve(BinWs* w, void* base, int64_t n, int32_t n_splits, int32_t d_bin, i
     w->counters = (unsigned*)take(sizeof(unsigned) * 4);
     w->medium = (int32_t*)take(sizeof(int32_t) * (size_t)w->list_cap);
     w->big = (int32_t*)take(sizeof(int32_t) * (size_t)w->list_cap);
+    w->rank = (int32_t*)take(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
     return align_up(off, 256);
 }
 
@@ -170,17 +175,30 @@ __global__ void __launch_bounds__(256) k_assign(const T* __restrict__ coords, in
                                                 const double* __restrict__ mins,
                                                 const double* __restrict__ widths,
                                                 int64_t* __restrict__ bin_idx,
-                                                int32_t* __restrict__ hist) {
+                                                int32_t* __restrict__ hist,
+                                                int32_t* __restrict__ rank, bool vec4) {
     const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const bool live = v < n;
     unsigned long long g = ~0ull;
     if (live) {
         const int s = split_of(rs, n_splits, v);
+        T x[DB];
+        bool done = false;
+        if constexpr (sizeof(T) == 4 && DB == 4) {
+            if (vec4) {  // n_c == 4, 16-byte aligned rows: one load
+                const float4 t = __ldg(reinterpret_cast<const float4*>(coords) + v);
+                x[0] = t.x; x[1] = t.y; x[2] = t.z; x[3] = t.w;
+                done = true;
+            }
+        }
+        if (!done) {
+#pragma unroll
+            for (int d = 0; d < DB; ++d) x[d] = coords[v * n_c + d];
+        }
         int64_t flat = 0;
 #pragma unroll
         for (int d = 0; d < DB; ++d) {
-            const double x = (double)coords[v * n_c + d];
-            const double q = __ddiv_rn(__dsub_rn(x, mins[(int64_t)s * DB + d]),
+            const double q = __ddiv_rn(__dsub_rn((double)x[d], mins[(int64_t)s * DB + d]),
                                        widths[(int64_t)s * DB + d]);
             int64_t c = (int64_t)floor(q);
             c = c < 0 ? 0 : (c >= n_bins ? n_bins - 1 : c);
@@ -189,26 +207,17 @@ __global__ void __launch_bounds__(256) k_assign(const T* __restrict__ coords, in
         g = (unsigned long long)((int64_t)s * total + flat);
         bin_idx[v] = (int64_t)g;
     }
-    // warp-aggregated histogram: one atomic per distinct cell in the warp
-    const unsigned peers = __match_any_sync(FG_FULL_MASK, g);
-    if (live && (__ffs(peers) - 1) == lane_id()) atomicAdd(&hist[g], __popc(peers));
-}
-
-// ---------------------------------------------------------------- K4
-__global__ void __launch_bounds__(256) k_scatter(const int64_t* __restrict__ bin_idx, int64_t n,
-                                                 int32_t* __restrict__ cursor,
-                                                 int32_t* __restrict__ sort_order) {
-    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const bool live = v < n;
-    const unsigned long long g = live ? (unsigned long long)bin_idx[v] : ~0ull;
+    // warp-aggregated histogram: one returning atomic per distinct cell in the
+    // warp; the old count + the lane's rank among its peers = arrival rank
     const unsigned peers = __match_any_sync(FG_FULL_MASK, g);
     const int leader = __ffs(peers) - 1;
     int32_t base = 0;
-    if (live && leader == lane_id()) base = atomicAdd(&cursor[g], __popc(peers));
+    if (live && leader == lane_id()) base = atomicAdd(&hist[g], __popc(peers));
     base = __shfl_sync(FG_FULL_MASK, base, leader);
-    if (live) sort_order[base + __popc(peers & lanemask_lt())] = (int32_t)v;
+    if (live) rank[v] = base + __popc(peers & lanemask_lt());
 }
 
+// ---------------------------------------------------------------- K4
 template <int NV, typename T>
 __device__ __forceinline__ void gather_row(const T* __restrict__ coords, int n_c, int32_t v,
                                            float4* __restrict__ dst) {
@@ -222,7 +231,25 @@ __device__ __forceinline__ void gather_row(const T* __restrict__ coords, int n_c
     }
 }
 
-// Thread per cell: sort segments of <= 32 ids (insertion sort), gather coords;
+// Vertex v -> slot bin_bounds[cell] + arrival rank: sort_order and the
+// coordinates (read coalesced) land in one pass; cells whose arrival order is
+// not the id order are fixed below.
+template <int NV, typename T>
+__global__ void __launch_bounds__(256) k_place(const int64_t* __restrict__ bin_idx,
+                                               const int32_t* __restrict__ rank,
+                                               const int32_t* __restrict__ bounds, int64_t n,
+                                               const T* __restrict__ coords, int n_c,
+                                               int32_t* __restrict__ sort_order,
+                                               float4* __restrict__ sorted) {
+    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const int32_t p = bounds[bin_idx[v]] + rank[v];
+    sort_order[p] = (int32_t)v;
+    gather_row<NV>(coords, n_c, (int32_t)v, sorted + (int64_t)p * NV);
+}
+
+// Thread per cell: sort segments of <= 32 ids (insertion sort) and re-gather
+// the ones that were out of order;
 // longer segments are queued for the CTA-level fix-ups.
 template <int NV, typename T>
 __global__ void __launch_bounds__(256) k_fix_small(const int32_t* __restrict__ bounds, int64_t n_cells,
@@ -244,9 +271,12 @@ __global__ void __launch_bounds__(256) k_fix_small(const int32_t* __restrict__ b
             medium[atomicAdd(&counters[1], 1u)] = (int32_t)c;
         return;
     }
+    if (len == 1) return;  // k_place wrote it
     int32_t ids[kSmallCell];
+    bool sorted_in = true;
     for (int i = 0; i < len; ++i) {
         int32_t x = sort_order[lo + i];
+        sorted_in &= i == 0 || ids[i - 1] < x;
         int j = i;
         while (j > 0 && ids[j - 1] > x) {
             ids[j] = ids[j - 1];
@@ -254,6 +284,7 @@ __global__ void __launch_bounds__(256) k_fix_small(const int32_t* __restrict__ b
         }
         ids[j] = x;
     }
+    if (sorted_in) return;  // arrival order == id order: k_place wrote it
     for (int i = 0; i < len; ++i) {
         sort_order[lo + i] = ids[i];
         gather_row<NV>(coords, n_c, ids[i], sorted + (int64_t)(lo + i) * NV);
@@ -364,10 +395,15 @@ k_fix_big(const int32_t* __restrict__ bounds, const int64_t* __restrict__ bin_id
 }
 
 template <int NV, typename T>
-int launch_fixups(const int32_t* bounds, int64_t n_cells, int32_t* sort_order, const int64_t* bin_idx,
+int launch_fixups(const int32_t* bounds, int64_t n, int64_t n_cells, int32_t* sort_order, const int64_t* bin_idx,
                   const int64_t* rs, int64_t total, const T* coords, int n_c, float* sorted,
                   const BinWs& w, cudaStream_t st) {
     float4* s4 = reinterpret_cast<float4*>(sorted);
+    if (n > 0) {
+        k_place<NV, T><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(bin_idx, w.rank, bounds, n, coords,
+                                                                  n_c, sort_order, s4);
+        FG_TRY(launched(st));
+    }
     if (n_cells > 0) {
         k_fix_small<NV, T><<<(unsigned)ceil_div(n_cells, 256), 256, 0, st>>>(
             bounds, n_cells, sort_order, coords, n_c, s4, w.counters, w.medium, w.big);
@@ -398,8 +434,10 @@ int launch_bin_core(const T* coords, int64_t n, int n_c, const int64_t* rs, int 
         w.bbox, rs, n_splits, DB, n_bins, mins, widths);
     FG_TRY(launched(st));
     if (n > 0) {
+        const bool vec4 = n_c == 4 && (reinterpret_cast<uintptr_t>(coords) & 15) == 0;
         k_assign<T, DB><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
-            coords, n, n_c, rs, n_splits, n_bins, total, mins, widths, bin_idx, w.cursor);
+            coords, n, n_c, rs, n_splits, n_bins, total, mins, widths, bin_idx, w.cursor, w.rank,
+            vec4);
         FG_TRY(launched(st));
     }
     return 0;
@@ -453,18 +491,16 @@ int bin_entry(const T* coords, int64_t n, int32_t n_coords, const int64_t* row_s
         case 4: FG_TRY((launch_bin_core<T, 4>(coords, n, n_coords, row_splits, n_splits, n_bins, total, dim_mins, widths, bin_idx, w, st))); break;
         default: FG_TRY((launch_bin_core<T, 5>(coords, n, n_coords, row_splits, n_splits, n_bins, total, dim_mins, widths, bin_idx, w, st))); break;
     }
-    fg::k_scan<<<(unsigned)w.n_tiles, kScanThreads, 0, st>>>(w.cursor, n_cells, bin_bounds, w.cursor,
+    fg::k_scan<<<(unsigned)w.n_tiles, kScanThreads, 0, st>>>(w.cursor, n_cells, bin_bounds, nullptr,
                                                         w.st, w.counters);
     FG_TRY(launched(st));
     if (n == 0) return 0;
-    k_scatter<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(bin_idx, n, w.cursor, sort_order);
-    FG_TRY(launched(st));
     const int nv = (n_coords + 3) / 4;
     switch (nv) {
-        case 1: return launch_fixups<1, T>(bin_bounds, n_cells, sort_order, bin_idx, row_splits, total, coords, n_coords, sorted_coords, w, st);
-        case 2: return launch_fixups<2, T>(bin_bounds, n_cells, sort_order, bin_idx, row_splits, total, coords, n_coords, sorted_coords, w, st);
-        case 3: return launch_fixups<3, T>(bin_bounds, n_cells, sort_order, bin_idx, row_splits, total, coords, n_coords, sorted_coords, w, st);
-        default: return launch_fixups<4, T>(bin_bounds, n_cells, sort_order, bin_idx, row_splits, total, coords, n_coords, sorted_coords, w, st);
+        case 1: return launch_fixups<1, T>(bin_bounds, n, n_cells, sort_order, bin_idx, row_splits, total, coords, n_coords, sorted_coords, w, st);
+        case 2: return launch_fixups<2, T>(bin_bounds, n, n_cells, sort_order, bin_idx, row_splits, total, coords, n_coords, sorted_coords, w, st);
+        case 3: return launch_fixups<3, T>(bin_bounds, n, n_cells, sort_order, bin_idx, row_splits, total, coords, n_coords, sorted_coords, w, st);
+        default: return launch_fixups<4, T>(bin_bounds, n, n_cells, sort_order, bin_idx, row_splits, total, coords, n_coords, sorted_coords, w, st);
     }
 }
 }  // namespace

@@ -9,16 +9,20 @@ namespace fg {
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 16;
 constexpr int kScanTile = kScanThreads * kScanItems;
+// shared-memory slot of tile item i: one pad word per 32 items, so the
+// thread-contiguous reads (thread t, items 16t..16t+15) hit 32 distinct banks
+// (unpadded they were 16-way conflicts) and the strided copies stay conflict-free
+__device__ __forceinline__ int scan_slot(int i) { return i + (i >> 5); }
 
-// Exclusive scan of hist[0..m) into out[0..m] (out[m] = grand total) and a
-// copy into cursor[0..m). Status word: bits 62-63 flag (0 invalid, 1 tile
+// Exclusive scan of hist[0..m) into out[0..m] (out[m] = grand total) and,
+// when cursor is not null, a copy into cursor[0..m). Status word: bits 62-63 flag (0 invalid, 1 tile
 // aggregate, 2 inclusive prefix), low 32 bits the value.
 static __global__ void __launch_bounds__(kScanThreads) k_scan(const int32_t* __restrict__ hist, int64_t m,
                                                        int32_t* __restrict__ out,
                                                        int32_t* __restrict__ cursor,
                                                        unsigned long long* __restrict__ status,
                                                        unsigned* __restrict__ ticket) {
-    __shared__ int32_t s_items[kScanTile];
+    __shared__ int32_t s_items[kScanTile + kScanTile / 32];
     __shared__ int32_t s_warp[kScanThreads / 32];
     __shared__ int32_t s_prefix;
     __shared__ unsigned s_tile;
@@ -28,7 +32,7 @@ static __global__ void __launch_bounds__(kScanThreads) k_scan(const int32_t* __r
     const int64_t base = tile * kScanTile;
     for (int i = threadIdx.x; i < kScanTile; i += kScanThreads) {
         const int64_t g = base + i;
-        s_items[i] = g < m ? hist[g] : 0;
+        s_items[scan_slot(i)] = g < m ? hist[g] : 0;
     }
     __syncthreads();
     int32_t local[kScanItems];
@@ -36,7 +40,7 @@ static __global__ void __launch_bounds__(kScanThreads) k_scan(const int32_t* __r
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) {
         local[j] = run;  // exclusive within the thread
-        run += s_items[threadIdx.x * kScanItems + j];
+        run += s_items[scan_slot(threadIdx.x * kScanItems + j)];
     }
     const int lane = lane_id(), w = threadIdx.x >> 5;
     const int32_t incl = warp_inclusive_scan(run);
@@ -99,13 +103,14 @@ static __global__ void __launch_bounds__(kScanThreads) k_scan(const int32_t* __r
     __syncthreads();
     const int32_t pre = s_prefix + thread_excl;
 #pragma unroll
-    for (int j = 0; j < kScanItems; ++j) s_items[threadIdx.x * kScanItems + j] = pre + local[j];
+    for (int j = 0; j < kScanItems; ++j) s_items[scan_slot(threadIdx.x * kScanItems + j)] = pre + local[j];
     __syncthreads();
     for (int i = threadIdx.x; i < kScanTile; i += kScanThreads) {
         const int64_t g = base + i;
         if (g < m) {
-            out[g] = s_items[i];
-            cursor[g] = s_items[i];
+            const int32_t x = s_items[scan_slot(i)];
+            out[g] = x;
+            if (cursor) cursor[g] = x;
         }
     }
     if (base + kScanTile >= m && threadIdx.x == 0) out[m] = s_prefix + tile_total;
