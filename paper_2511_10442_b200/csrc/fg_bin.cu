@@ -37,6 +37,7 @@ constexpr int kMediumCell = 4096;
 
 struct BinWs {
     unsigned long long* bbox;  // n_splits * d_bin * 2 (ordered-double min, max)
+    double* inv_w;           // n_splits * d_bin: RN(1 / width), the cell fast path
     int32_t* cursor;         // n_cells (histogram, then scatter cursor)
     unsigned long long* st;  // scan tile status words
     unsigned* counters;      // [0] scan tile ticket, [1] medium count, [2] big count
@@ -59,6 +60,7 @@ size_t carve(BinWs* w, void* base, int64_t n, int32_t n_splits, int32_t d_bin, i
     w->n_tiles = ceil_div(n_cells, kScanTile);
     w->list_cap = n / (kSmallCell + 1) + 1;
     w->bbox = (unsigned long long*)take(sizeof(unsigned long long) * (size_t)n_splits * d_bin * 2);
+    w->inv_w = (double*)take(sizeof(double) * (size_t)n_splits * d_bin);
     w->cursor = (int32_t*)take(sizeof(int32_t) * (size_t)n_cells);
     w->st = (unsigned long long*)take(sizeof(unsigned long long) * (size_t)w->n_tiles);
     w->counters = (unsigned*)take(sizeof(unsigned) * 4);
@@ -151,20 +153,23 @@ __global__ void __launch_bounds__(256) k_bbox(const T* __restrict__ coords, int6
 // pyx:99-118: empty split keeps min 0 / width 1; width = ext / n_bins or 1.0.
 __global__ void k_bbox_final(const unsigned long long* __restrict__ bbox, const int64_t* __restrict__ rs,
                              int n_splits, int d_bin, int n_bins, double* __restrict__ mins,
-                             double* __restrict__ widths) {
+                             double* __restrict__ widths, double* __restrict__ inv_w) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= (int64_t)n_splits * d_bin) return;
     const int64_t s = i / d_bin;
     if (rs[s + 1] <= rs[s]) {
         mins[i] = 0.0;
         widths[i] = 1.0;
+        inv_w[i] = 1.0;
         return;
     }
     const double mn = ordered_to_double(bbox[i * 2 + 0]);
     const double mx = ordered_to_double(bbox[i * 2 + 1]);
     const double ext = __dsub_rn(mx, mn);
+    const double w = ext > 0.0 ? __ddiv_rn(ext, (double)n_bins) : 1.0;
     mins[i] = mn;
-    widths[i] = ext > 0.0 ? __ddiv_rn(ext, (double)n_bins) : 1.0;
+    widths[i] = w;
+    inv_w[i] = __drcp_rn(w);
 }
 
 // ---------------------------------------------------------------- K2
@@ -174,6 +179,7 @@ __global__ void __launch_bounds__(256) k_assign(const T* __restrict__ coords, in
                                                 int n_bins, int64_t total,
                                                 const double* __restrict__ mins,
                                                 const double* __restrict__ widths,
+                                                const double* __restrict__ inv_w,
                                                 int64_t* __restrict__ bin_idx,
                                                 int32_t* __restrict__ hist,
                                                 int32_t* __restrict__ rank, bool vec4) {
@@ -198,8 +204,18 @@ __global__ void __launch_bounds__(256) k_assign(const T* __restrict__ coords, in
         int64_t flat = 0;
 #pragma unroll
         for (int d = 0; d < DB; ++d) {
-            const double q = __ddiv_rn(__dsub_rn((double)x[d], mins[(int64_t)s * DB + d]),
-                                       widths[(int64_t)s * DB + d]);
+            // floor(RN(a / w)) exactly as the reference, without the division in
+            // the common case: q1 = RN(a * RN(1/w)) is within 3.02u|q1| of RN(a/w)
+            // (u = 2^-53), so when no integer lies within 5e-16|q1| of q1 both
+            // floor the same; otherwise (cell edges, q = 0, the top edge,
+            // non-finite values) the exact division decides.
+            const double a = __dsub_rn((double)x[d], mins[(int64_t)s * DB + d]);
+            const double q1 = __dmul_rn(a, inv_w[(int64_t)s * DB + d]);
+            const double f1 = floor(q1);
+            const double eps = 5e-16 * fabs(q1);
+            const double q = (q1 - f1 > eps && (f1 + 1.0) - q1 > eps)
+                                 ? q1
+                                 : __ddiv_rn(a, widths[(int64_t)s * DB + d]);
             int64_t c = (int64_t)floor(q);
             c = c < 0 ? 0 : (c >= n_bins ? n_bins - 1 : c);
             flat = flat * n_bins + c;
@@ -234,6 +250,7 @@ __device__ __forceinline__ void gather_row(const T* __restrict__ coords, int n_c
 // Vertex v -> slot bin_bounds[cell] + arrival rank: sort_order and the
 // coordinates (read coalesced) land in one pass; cells whose arrival order is
 // not the id order are fixed below.
+constexpr int kPlacePer = 4;  // vertices per thread: their loads are in flight together
 template <int NV, typename T>
 __global__ void __launch_bounds__(256) k_place(const int64_t* __restrict__ bin_idx,
                                                const int32_t* __restrict__ rank,
@@ -241,11 +258,24 @@ __global__ void __launch_bounds__(256) k_place(const int64_t* __restrict__ bin_i
                                                const T* __restrict__ coords, int n_c,
                                                int32_t* __restrict__ sort_order,
                                                float4* __restrict__ sorted) {
-    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (v >= n) return;
-    const int32_t p = bounds[bin_idx[v]] + rank[v];
-    sort_order[p] = (int32_t)v;
-    gather_row<NV>(coords, n_c, (int32_t)v, sorted + (int64_t)p * NV);
+    const int64_t v0 = (int64_t)blockIdx.x * (256 * kPlacePer) + threadIdx.x;
+    int64_t g[kPlacePer];
+    int32_t r[kPlacePer], p[kPlacePer];
+#pragma unroll
+    for (int j = 0; j < kPlacePer; ++j) {
+        const int64_t v = v0 + 256 * j;
+        g[j] = v < n ? __ldcs(bin_idx + v) : -1;
+        r[j] = v < n ? __ldcs(rank + v) : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < kPlacePer; ++j) p[j] = g[j] >= 0 ? __ldg(bounds + g[j]) + r[j] : -1;
+#pragma unroll
+    for (int j = 0; j < kPlacePer; ++j) {
+        if (p[j] < 0) continue;
+        const int64_t v = v0 + 256 * j;
+        sort_order[p[j]] = (int32_t)v;
+        gather_row<NV>(coords, n_c, (int32_t)v, sorted + (int64_t)p[j] * NV);
+    }
 }
 
 // Thread per cell: sort segments of <= 32 ids (insertion sort) and re-gather
@@ -400,7 +430,7 @@ int launch_fixups(const int32_t* bounds, int64_t n, int64_t n_cells, int32_t* so
                   const BinWs& w, cudaStream_t st) {
     float4* s4 = reinterpret_cast<float4*>(sorted);
     if (n > 0) {
-        k_place<NV, T><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(bin_idx, w.rank, bounds, n, coords,
+        k_place<NV, T><<<(unsigned)ceil_div(n, 256 * kPlacePer), 256, 0, st>>>(bin_idx, w.rank, bounds, n, coords,
                                                                   n_c, sort_order, s4);
         FG_TRY(launched(st));
     }
@@ -431,12 +461,12 @@ int launch_bin_core(const T* coords, int64_t n, int n_c, const int64_t* rs, int 
         FG_TRY(launched(st));
     }
     k_bbox_final<<<(unsigned)ceil_div((int64_t)n_splits * DB, 128), 128, 0, st>>>(
-        w.bbox, rs, n_splits, DB, n_bins, mins, widths);
+        w.bbox, rs, n_splits, DB, n_bins, mins, widths, w.inv_w);
     FG_TRY(launched(st));
     if (n > 0) {
         const bool vec4 = n_c == 4 && (reinterpret_cast<uintptr_t>(coords) & 15) == 0;
         k_assign<T, DB><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
-            coords, n, n_c, rs, n_splits, n_bins, total, mins, widths, bin_idx, w.cursor, w.rank,
+            coords, n, n_c, rs, n_splits, n_bins, total, mins, widths, w.inv_w, bin_idx, w.cursor, w.rank,
             vec4);
         FG_TRY(launched(st));
     }
