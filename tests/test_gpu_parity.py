@@ -137,6 +137,37 @@ def test_bin_clustered_config_b_vs_oracle(oracle):
     assert np.array_equal(got[5][:, :n_c], c[ref[1]])
 
 
+def test_bin_cell_edges_vs_oracle(oracle):
+    """Coordinates on and one ulp either side of cell edges (the cases where the
+    cell index falls back from RN(a * RN(1/w)) to the exact division), several
+    n_bins (powers of two: exact quotients; odd: inexact widths), float32 and
+    float64 inputs -- bin arrays equal to the oracle's."""
+    rng = np.random.default_rng(11)
+    for n_bins in (8, 13, 29, 64):
+        edges = np.arange(n_bins + 1, dtype=np.float64) / n_bins
+        base = rng.choice(edges, size=(6000, 4))
+        nudge = rng.integers(-1, 2, size=base.shape)
+        c32 = base.astype(np.float32)
+        c32 = np.where(nudge > 0, np.nextafter(c32, np.float32(2)),
+                       np.where(nudge < 0, np.nextafter(c32, np.float32(-1)), c32))
+        c32[0] = 0.0
+        c32[1] = 1.0
+        c32 = np.concatenate([c32, rng.random((2000, 4)).astype(np.float32)])
+        off = np.array([0, 3000, len(c32)], np.int64)
+        ref = oracle.build_index(c32.astype(np.float64), off, 4, n_bins)
+        got = run_bin(c32, off, 4, n_bins)
+        for r, g_ in zip(ref, got[:5]):
+            assert np.array_equal(r, g_.astype(r.dtype))
+        b64 = np.where(nudge > 0, np.nextafter(base, 2.0),
+                       np.where(nudge < 0, np.nextafter(base, -1.0), base))
+        c64 = np.concatenate([b64, rng.random((2000, 4))])
+        got64 = [o.cpu().numpy() for o in ops.bin_by_coordinates(
+            t(c64, torch.float64), t(off, torch.int64), 4, n_bins)]
+        ref64 = oracle.build_index(c64, off, 4, n_bins)
+        for r, g_ in zip(ref64, got64[:5]):
+            assert np.array_equal(r, g_.astype(r.dtype))
+
+
 def test_bin_fp64_cell_kat():
     # SURVEY App. B: generate_dataset(1_000_000, 4, seed=1) as f32, vertex 842094,
     # dim 3: float64 cell arithmetic gives 28 (float32 would give 27).
