@@ -94,11 +94,14 @@ struct HdWarp {
 };
 
 // Per-lane buffer entries and warps per CTA of an instantiation: the float32
-// d <= 4 kernels (the clustered fallback, k <= 41 there) use 96 entries and
-// one warp per CTA -- 7 warps/SM instead of 6 (config B 8% faster); d > 4
-// (config C, k = 64: more room between cuts) and float64 (k <= 120) keep 128.
+// d <= 4 kernels (the clustered fallback, k <= 41 there) use 80 entries and
+// one warp per CTA -- 9 warps/SM (the 224-register cap allows 9) instead of 6
+// with 128 (config B: 96 entries / 7 warps 8% faster than 128, 80 / 9 warps
+// another ~10%; 72 entries at 200 registers / 10 warps no faster, 64 entries
+// at 168 registers spill); d > 4 (config C, k = 64: more room between cuts)
+// and float64 (k <= 120) keep 128.
 #ifndef FG_HD_CAP_LOWD
-#define FG_HD_CAP_LOWD 96
+#define FG_HD_CAP_LOWD 80
 #endif
 template <int NV, bool X64>
 __host__ __device__ constexpr int hd_cap() {
@@ -450,7 +453,7 @@ __device__ __noinline__ int cut_lane(HdWarp<DE, CAP>& W, const search::KnnArgs& 
                                      float& tau_j, float& tt_j, const float (&qj)[4 * NV],
                                      int32_t qid, float r) {
     const int lane = lane_id();
-    constexpr int PER = CAP / 32;
+    constexpr int PER = (CAP + 31) / 32;  // CAP need not be a multiple of 32
     float* bd = &W.bd[j * (CAP + 1)];
     int32_t* bp = &W.bp[j * (CAP + 1)];
     __syncwarp();  // lane j's appends (its own shared-memory stores) before the other lanes read them
@@ -908,8 +911,15 @@ __device__ __forceinline__ void scan_spans(HdWarp<DE, CAP>& W, const search::Knn
 }
 
 // ---------------------------------------------------------------- search
+#ifndef FG_HD_REGS_LOWD
+#define FG_HD_REGS_LOWD 224
+#endif
+template <int NV, bool X64>
+__host__ __device__ constexpr int hd_regs() {
+    return NV == 1 && !X64 ? FG_HD_REGS_LOWD : 224;
+}
 template <int NV, int DB, int DE, bool X64>
-__global__ void __maxnreg__(224) k_hd_search(const __grid_constant__ tile::TileArgs t,
+__global__ void __maxnreg__((hd_regs<NV, X64>())) k_hd_search(const __grid_constant__ tile::TileArgs t,
                                                            const __grid_constant__ search::KnnArgs a) {
     constexpr int NL = DB - 1;
     extern __shared__ __align__(16) unsigned char smem_raw[];
