@@ -1241,12 +1241,26 @@ __device__ __forceinline__ unsigned morton_spread(unsigned x, int dims, int bits
     return r;
 }
 
+// One CTA per dense cell: the cell's points ordered by the top B bits of their
+// in-cell Morton code (B ~ log2(len) - 1: about two points per bucket), by a
+// counting sort -- shared-memory histogram, block scan, atomic scatter, then
+// each bucket put in index order by a thread (the order is deterministic; the
+// buckets are small) -- 5 barriers per cell instead of the ~100 of a bitonic
+// sort of 16384 keys (config B: 185 -> 50 us).  Only the compactness of
+// the search's tiles depends on this order, never the answer.
+constexpr int kMortonBuckets = 4096;
 template <int NV, int DB>
 __global__ void __launch_bounds__(1024) k_dense_morton(const tile::TileArgs t) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    unsigned long long* key = reinterpret_cast<unsigned long long*>(smem_raw);  // (morton << 32) | i
+    uint16_t* bk = reinterpret_cast<uint16_t*>(smem_raw);          // bucket of entry i
+    uint16_t* perm = bk + kMaxSortCell;                            // entries by bucket
+    int32_t* cur = reinterpret_cast<int32_t*>(perm + kMaxSortCell);  // counts -> cursors
+    int32_t* start = cur + kMortonBuckets;                         // bucket starts (+ total)
+    __shared__ int32_t s_warp[32];
     constexpr int bits = 32 / DB > 10 ? 10 : 32 / DB;
+    constexpr int TB = DB * bits;  // Morton code bits
     if (tile::gated_off(t)) return;
+    const int lane = lane_id(), w = threadIdx.x >> 5;
     const int count = t.ctr[5];
     for (int it = blockIdx.x; it < count; it += gridDim.x) {
         const int32_t c = t.dense[it];
@@ -1259,41 +1273,69 @@ __global__ void __launch_bounds__(1024) k_dense_morton(const tile::TileArgs t) {
             cell[i] = (int)(flat % t.nb);
             flat /= t.nb;
         }
-        int p2 = 64;
-        while (p2 < len) p2 <<= 1;
-        for (int i = threadIdx.x; i < p2; i += blockDim.x) {
-            unsigned long long kk = ~0ull;
-            if (i < len) {
-                const float4 x = t.sc[(int64_t)(lo + i) * NV];
-                const float xa[4] = {x.x, x.y, x.z, x.w};
-                unsigned mk = 0;
+        const int B = min(min(12, TB), max(1, 31 - __clz(len)));  // ~2 points per bucket
+        const int NB = 1 << B;
+        for (int b = threadIdx.x; b < NB; b += blockDim.x) cur[b] = 0;
+        __syncthreads();
+        for (int i = threadIdx.x; i < len; i += blockDim.x) {
+            const float4 x = t.sc[(int64_t)(lo + i) * NV];
+            const float xa[4] = {x.x, x.y, x.z, x.w};
+            unsigned mk = 0;
 #pragma unroll
-                for (int d = 0; d < DB && d < 4; ++d) {
-                    const double w = t.widths[s * DB + d];
-                    const double u = ((double)xa[d] - (t.mins[s * DB + d] + cell[d] * w)) / w;
-                    const int qd = min((1 << bits) - 1, max(0, (int)(u * (1 << bits))));
-                    mk |= morton_spread((unsigned)qd, DB, bits) << d;
-                }
-                kk = ((unsigned long long)mk << 32) | (unsigned)i;
+            for (int d = 0; d < DB && d < 4; ++d) {
+                const double wd = t.widths[s * DB + d];
+                const double u = ((double)xa[d] - (t.mins[s * DB + d] + cell[d] * wd)) / wd;
+                const int qd = min((1 << bits) - 1, max(0, (int)(u * (1 << bits))));
+                mk |= morton_spread((unsigned)qd, DB, bits) << d;
             }
-            key[i] = kk;
+            const int b = (int)(mk >> (TB - B));
+            bk[i] = (uint16_t)b;
+            atomicAdd(&cur[b], 1);
         }
         __syncthreads();
-        for (int size = 2; size <= p2; size <<= 1)
-            for (int stride = size >> 1; stride > 0; stride >>= 1) {
-                for (int i = threadIdx.x; i < p2 / 2; i += blockDim.x) {
-                    const int x0 = ((i & ~(stride - 1)) << 1) | (i & (stride - 1)), x1 = x0 + stride;  // stride: a power of 2
-                    const bool up = (x0 & size) == 0;
-                    const unsigned long long ka = key[x0], kb = key[x1];
-                    if ((ka > kb) == up) {
-                        key[x0] = kb;
-                        key[x1] = ka;
-                    }
-                }
-                __syncthreads();
+        {  // exclusive scan of the NB <= 4096 counts: 4 per thread
+            int v[4], tot = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int b = 4 * threadIdx.x + j;
+                v[j] = b < NB ? cur[b] : 0;
+                tot += v[j];
             }
+            const int incl = warp_inclusive_scan(tot);
+            if (lane == 31) s_warp[w] = incl;
+            __syncthreads();
+            if (w == 0) s_warp[lane] = warp_inclusive_scan(s_warp[lane]);
+            __syncthreads();
+            int run = incl - tot + (w > 0 ? s_warp[w - 1] : 0);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int b = 4 * threadIdx.x + j;
+                if (b < NB) {
+                    start[b] = run;
+                    cur[b] = run;
+                }
+                run += v[j];
+            }
+            if (threadIdx.x == 0) start[NB] = len;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < len; i += blockDim.x) perm[atomicAdd(&cur[bk[i]], 1)] = (uint16_t)i;
+        __syncthreads();
+        for (int b = threadIdx.x; b < NB; b += blockDim.x) {  // index order inside each bucket
+            const int b0 = start[b], b1 = start[b + 1];
+            for (int i = b0 + 1; i < b1; ++i) {
+                const uint16_t x = perm[i];
+                int j = i;
+                while (j > b0 && perm[j - 1] > x) {
+                    perm[j] = perm[j - 1];
+                    --j;
+                }
+                perm[j] = x;
+            }
+        }
+        __syncthreads();
         for (int j = threadIdx.x; j < len; j += blockDim.x) {
-            const int src = (int)(key[j] & 0xffffffffu);
+            const int src = perm[j];
 #pragma unroll
             for (int v = 0; v < NV; ++v) t.sc2[(int64_t)(lo + j) * NV + v] = t.sc[(int64_t)(lo + src) * NV + v];
             t.sid2[lo + j] = t.sid[lo + src];
@@ -1335,7 +1377,7 @@ int launch_hd(tile::TileArgs& t_in, const search::KnnArgs& a_in, cudaStream_t st
         const int64_t n_cells = (int64_t)t.n_blocks / t.bps * t.total;
         k_cell_split<NV><<<(unsigned)ceil_div(n_cells, 256), 256, 0, st>>>(t, n_cells);
         FG_TRY(launched(st));
-        const size_t msmem = sizeof(unsigned long long) * kMaxSortCell;
+        const size_t msmem = 2 * sizeof(uint16_t) * kMaxSortCell + sizeof(int32_t) * (2 * kMortonBuckets + 1);
         FG_CUDA(cudaFuncSetAttribute(k_dense_morton<NV, DB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)msmem));
         k_dense_morton<NV, DB><<<(unsigned)sms, 1024, msmem, st>>>(t);
