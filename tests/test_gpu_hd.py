@@ -124,3 +124,44 @@ def test_clustered_fallback_equals_warp_kernel(n, d, k, splits):
     assert_rows(gi, gd, wi, wd, "clustered fallback vs warp-per-query")
     bi, bd = brute(c32, off, k)
     assert_rows(gi, gd, bi, bd.astype(np.float32), "clustered fallback vs brute")
+
+
+def test_clustered_fallback_dense_cell_sizes(oracle):
+    """Cells of exactly 33, 4096, 16384 (kMaxSortCell: the largest the dense-cell
+    counting sort orders) and 16385 points (kept in binning order) over a uniform
+    background: bin arrays equal to the oracle's (medium and big-cell fix-ups),
+    every neighbour row equal to the brute force."""
+    rng = np.random.default_rng(5)
+    k, d = 40, 4
+    bg = rng.random((20_000, d))
+    bg[0], bg[1] = 0.0, 1.0  # extents exactly [0, 1]: widths 1 / n_bins
+    sizes = [33, 4096, 16384, 16385]
+    n = bg.shape[0] + sum(sizes)
+    nb = fg.compute_n_bins(n, k, d)
+    cells = [np.array([2 + 3 * j, 5, 7, 9]) % nb for j in range(len(sizes))]
+    bc = np.floor(bg * nb).astype(np.int64)
+    keep = np.ones(len(bg), bool)
+    for cl in cells:  # the blob cells hold the blob points only
+        keep &= ~(bc == cl).all(1)
+    keep[:2] = True
+    parts = [bg[keep]]
+    for cl, m in zip(cells, sizes):
+        parts.append((cl + 0.5) / nb + (rng.random((m, d)) - 0.5) * (0.4 / nb))
+    c32 = np.concatenate(parts).astype(np.float32)
+    n = c32.shape[0]
+    off = np.array([0, n], np.int64)
+    assert fg.compute_n_bins(n, k, d) == nb
+    ref = oracle.build_index(c32.astype(np.float64), off, d, nb)
+    L = np.diff(ref[2])
+    for m in sizes:
+        assert (L == m).any(), f"no cell holds exactly {m} points"
+    ct = torch.from_numpy(c32).cuda()
+    rs = torch.from_numpy(off).cuda()
+    got = [o.cpu().numpy() for o in ops.bin_by_coordinates(ct, rs, d, nb)]
+    for r, g_ in zip(ref, got[:5]):
+        assert np.array_equal(r, g_.astype(r.dtype))
+    search(c32, off, k, d)  # a clustered call: the next one launches the fallback
+    gi, gd, st = search(c32, off, k, d, stats=True)
+    assert st["hd_tiles"] > 0, "the clustered fallback did not run"
+    bi, bd = brute(c32, off, k)
+    assert_rows(gi, gd, bi, bd.astype(np.float32), "dense cells vs brute")
