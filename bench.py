@@ -190,7 +190,8 @@ def config_keys(config, n, d, k, n_bins, events, flushed):
     """The workload description shared by both arms (same keys)."""
     return {"workload": DESC[config], "n_points_per_gpu": n, "d": d, "k": k, "n_bins": n_bins,
             "d_bin": min(d, 5), "events": events,
-            "l2": "flushed (256 MiB write) before every step" if flushed else "no flush"}
+            "l2": ("GPU arm: L2 flushed (256 MiB write) before every step; CPU reference arm: "
+                   "no flush") if flushed else "no flush"}
 
 
 def cpu_reference_step(coords32, offsets, k, n_bins, query_frac=1.0, bwd_rows=100_000, seed=0):
@@ -266,7 +267,11 @@ def run_reference(args):
             "ms_per_step": float(np.mean(times)) * 1e3, "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference generate_dataset)",
-            "config": config_keys(args.config, n, d, k, n_bins, len(off) - 1, False),
+            # same keys and values as the GPU arm's line (weak scaling: one event
+            # per GPU; the host's rate is per query, so it covers N events alike)
+            "config": config_keys(args.config, n, d, k, n_bins,
+                                  max(args.gpus, 1) if scaling == "weak" else len(off) - 1,
+                                  not args.no_flush),
             "per_step": {"fwd_queries": det["fwd_queries"], "bwd_rows": det["bwd_rows"],
                          "us_per_query_fwd": float(np.mean(fwd_t)) * 1e6,
                          "us_per_row_bwd": float(np.mean(bwd_t)) * 1e6},
@@ -490,9 +495,11 @@ def main():
     # would: coordinates (+ features) first, the upstream gradients while the
     # search runs; the forward outputs go back while the backward runs.
     e2e = None
+    e2e_reps = []
     if not args.no_e2e:
         s_h2d = torch.cuda.Stream(dev)
         s_d2h = torch.cuda.Stream(dev)
+        copy_streams = [s_h2d, s_d2h]  # replaced per timed repetition (see below)
         h_first = [torch.from_numpy(coords_np).pin_memory()]
         h_late = [torch.from_numpy(up_np).pin_memory()] if not gravnet else [up_agg.cpu().pin_memory()]
         if gravnet:
@@ -501,6 +508,7 @@ def main():
         d_late = [torch.empty_like(h, device=dev) for h in h_late]
 
         def e2e_step(h_out=None, join=True):
+            s_h2d, s_d2h = copy_streams
             ev_first = torch.cuda.Event()
             ev_late = torch.cuda.Event()
             s_h2d.wait_stream(stream)
@@ -542,8 +550,10 @@ def main():
                     s_d2h.wait_event(ev_bwd)
                     for h_, o_ in zip(h_out[len(fwd_outs):], bwd_outs):
                         h_.copy_(o_, non_blocking=True)
-                for o_ in outs:  # the caching allocator must not recycle them early
-                    o_.record_stream(s_d2h)
+                # no record_stream: the caller keeps the outputs alive until `stream`
+                # has waited for their copies (join below, or pipelined()'s window),
+                # so the caching allocator recycles blocks in stream order without
+                # polling copy-stream events
                 if join:
                     stream.wait_stream(s_d2h)
             return outs
@@ -569,38 +579,47 @@ def main():
         # steps back to back, at most two in flight (step i waits for step i-2's
         # copies, so the caching allocator recycles output blocks)
         def pipelined(n_steps):
-            done = []
+            done, alive = [], []
             for it in range(n_steps):
                 if it >= 2:
                     stream.wait_event(done[it - 2])
+                    alive.pop(0)  # step it-2's outputs: their copies are ordered before `stream` now
                 if flush is not None:
                     flush.zero_()
-                e2e_step(h_out, join=False)
+                alive.append(e2e_step(h_out, join=False))
                 ev = torch.cuda.Event()
-                ev.record(s_d2h)
+                ev.record(copy_streams[1])
                 done.append(ev)
-            stream.wait_stream(s_d2h)
+            stream.wait_stream(copy_streams[1])
+            alive.clear()
 
-        # warm the back-to-back mode for >= 0.5 s (a short loop after an idle gap
-        # was once timed at lowered clocks: one-off 14-23 ms steps at config B)
-        t_w = time.perf_counter()
-        while True:
-            pipelined(3)
-            torch.cuda.synchronize()
-            if time.perf_counter() - t_w >= 0.5:
-                break
-        if world > 1:
-            dist.barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        pipelined(e2e_steps)
-        e1.record(stream)
-        e1.synchronize()
-        e2e_ms = e0.elapsed_time(e1) / e2e_steps
+        # back to back: three timed repetitions, each on fresh copy streams after
+        # >= 0.3 s of warm-up in that mode; the median is reported and every
+        # repetition listed (single runs were seen 1.6x slower than the rest:
+        # 10.5 vs 6.6 ms at north_star, 14 vs 4 ms at B -- copies serialised)
+        reps = []
+        for rep in range(3):
+            copy_streams[:] = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+            t_w = time.perf_counter()
+            while True:
+                pipelined(3)
+                torch.cuda.synchronize()
+                if time.perf_counter() - t_w >= 0.3:
+                    break
+            if world > 1:
+                dist.barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            pipelined(e2e_steps)
+            e1.record(stream)
+            e1.synchronize()
+            reps.append(e0.elapsed_time(e1) / e2e_steps)
+        e2e_ms = float(np.median(reps))
         h2d = sum(h.numel() * h.element_size() for h in h_first + h_late)
         d2h = sum(h.numel() * h.element_size() for h in h_out)
         e2e = [e2e_ms, h2d, d2h, lat_ms]
+        e2e_reps = reps
 
     per_rank = [t_step, n, e2e[0] if e2e else 0.0, e2e[3] if e2e else 0.0] + list(t_phase)
     allr = sharding.gather_floats(per_rank)
@@ -677,11 +696,12 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (reference generate_dataset, seed per rank, cast to float32)",
-        "config": {**config_keys(args.config, n, d, k, n_bins,
-                                 world if scaling == "weak" else 64, not args.no_flush),
-                   "precision": "fp32 distance filter, float64 exact epilogue / gradient terms",
-                   "backward": "deterministic transposed" if det else
-                               "compensated fp32x4 atomics (pipelined stream kernel for d = 4)"},
+        # the same config keys and values as the reference arm's line
+        "config": config_keys(args.config, n, d, k, n_bins,
+                              world if scaling == "weak" else 64, not args.no_flush),
+        "precision": "fp32 distance filter, float64 exact epilogue / gradient terms",
+        "backward_mode": "deterministic transposed" if det else
+                         "compensated fp32x4 atomics (pipelined stream kernel for d = 4)",
         "breakdown_ms": phase,
         "roofline": roof,
         "gpu_launches": int(launches),
@@ -696,7 +716,9 @@ def main():
                        "ms_per_step": e2e_ms,
                        "mode": "steps back to back (step i's outputs copy back while step i+1's "
                                "inputs arrive and it computes); every step moves all its bytes",
-                       "latency_ms_per_step": float(allr[:, 3].max())}
+                       "latency_ms_per_step": float(allr[:, 3].max()),
+                       "repetitions_ms_per_step": [round(float(x), 4) for x in e2e_reps],
+                       "statistic": "median of 3 timed repetitions (rank 0's list; max over ranks of the median)"}
     if world == 1 and not args.no_cpu_baseline:
         try:
             tt, rate, det_ = cpu_reference_step(coords_np, off_np, k, n_bins,
