@@ -35,7 +35,7 @@ namespace binning {
 
 constexpr int kMaxBinDims = 5;
 constexpr int kSmallCell = 32;
-constexpr int kMediumCell = 4096;
+constexpr int kMediumCell = 8192;  // CTA bitonic in 32 KB of shared memory (B: its 6 cells of 4.6-6.3k points)
 
 struct BinWs {
     unsigned long long* bbox;  // n_splits * d_bin * 2 (ordered-double min, max)
